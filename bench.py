@@ -1,0 +1,349 @@
+#!/usr/bin/env python
+"""Benchmark of the MERF baked-scene render path on B200 (one JSON line on rank 0).
+
+Workload (BASELINE.json metric "rays/sec and fps at 1920x1080 per B200"): the paper-scale
+synthetic baked MERF scene (512^3 block-sparse grid, 3 x 2048^2 planes, C = 8, occupancy
+32^3/128^3/256^3; config 2's scene) rendered from the config-4 orbit of 256 1920x1080 views.
+A step = every rank renders its V views (RGBA8) with the fused render kernel and, for N > 1,
+the finished frames are gathered to rank 0 over NCCL (the only collective; off the hot path).
+Weak scaling: V views per rank per step; rank r of N takes views (s*V*N + i*N + r) mod 256.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl merf|reference]
+
+`--impl reference` times the fp64 CPU oracle (the only "reference implementation" of this
+tier: the paper publishes no code) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "rays/sec and fps at 1920x1080 per B200 (1/2/4/8 GPUs); gather GB/s vs roofline"
+W_IMG, H_IMG = 1920, 1080
+N_ORBIT = 256
+BYTES_APPEARANCE = 160      # 20 texels x 8 channels x 1 B
+BYTES_DENSITY_ONLY = 20     # 20 texels x 1 B
+BYTES_OUT = 4               # RGBA8 per ray
+PAPER_CONTEXT = {"merf_fps_rtx3090_1080p_browser": 119, "merf_fps_m1_720p_browser": 28.3,
+                 "source": "PAPER.md Table 2 (P:379, P:383); real scenes, other hardware"}
+
+
+def views_for(rank: int, world: int, step: int, per_rank: int, n_orbit: int = N_ORBIT):
+    """view indices rank `rank` renders at step `step` (weak scaling: per_rank fixed)."""
+    return [(step * per_rank * world + i * world + rank) % n_orbit for i in range(per_rank)]
+
+
+def gather_frames(frames, rank: int, world: int, group=None):
+    """gather every rank's frame batch to rank 0 (NCCL on GPU, gloo in tests)."""
+    import torch
+    import torch.distributed as dist
+    if world == 1:
+        return [frames]
+    out = [torch.empty_like(frames) for _ in range(world)] if rank == 0 else None
+    dist.gather(frames, gather_list=out, dst=0, group=group)
+    return out
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            p = [x.strip() for x in line.split(",")]
+            if len(p) >= 6:
+                self.rows.append(p)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(2)
+        except Exception:
+            self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def _ncu_traffic():
+    """dram bytes per launch of the render kernel from the committed ncu --set full capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "render_traffic.json")) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def cpu_baseline(scene, cam, sample_stride: int = 1):
+    """the fp64 oracle, as it stands, on all host cores: one 1080p orbit view (or every
+    `sample_stride`-th pixel of it)."""
+    import numpy as np
+    from oracle import oracle as O
+    osc = O.OracleScene(scene)
+    pix = np.arange(0, W_IMG * H_IMG, sample_stride, dtype=np.int64)
+    t0 = time.perf_counter()
+    r = O.render(osc, cam, W_IMG, H_IMG, pixels=pix)
+    dt = time.perf_counter() - t0
+    return {"value": len(pix) / dt, "unit": "rays/s", "cores": O.max_threads(), "kind": "oracle",
+            "sample": f"{len(pix)} rays of orbit view 0 at 1920x1080 (every {sample_stride}th pixel), "
+                      f"fp64, {dt:.1f} s wall, samples/ray {r['stats']['evaluated'] / len(pix):.1f}",
+            "seconds": dt}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle on a bounded sample per step (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import numpy as np
+    from merf_inputs import make_scene, orbit_cameras
+    from oracle import oracle as O
+    sc = make_scene("c2")
+    osc = O.OracleScene(sc)
+    stride = 37     # ~56k rays per step: a step is ~1/37 of a view's pixels
+    times, rays = [], 0
+    for s in range(args.warmup + args.steps):
+        v = views_for(0, 1, s, 1)[0]
+        cam = orbit_cameras(N_ORBIT, indices=[v])[0]
+        pix = np.arange(s % stride, W_IMG * H_IMG, stride, dtype=np.int64)
+        t0 = time.perf_counter()
+        O.render(osc, cam, W_IMG, H_IMG, pixels=pix)
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            times.append(dt)
+            rays += len(pix)
+    total = sum(times)
+    value = rays / total
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "rays/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "orbit1080p_paper_scale_merf", "scene": "c2 (512^3 sparse grid, 3x2048^2 planes)",
+                       "sample": f"every {stride}th pixel of one 1920x1080 orbit view per step"},
+            "cpu_baseline": {"value": value, "unit": "rays/s", "cores": O.max_threads(), "kind": "oracle",
+                             "sample": f"every {stride}th pixel of one 1920x1080 orbit view per step"},
+            "e2e": {"value": value, "unit": "rays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "fps_equivalent": value / (W_IMG * H_IMG)}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="merf", choices=["merf", "reference"])
+    ap.add_argument("--views", type=int, default=16, help="views per rank per step")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from merf_inputs import make_scene, orbit_cameras
+    import paper_2302_12249_b200 as M
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    assert torch.cuda.is_available(), "bench.py needs a GPU (no CPU fallback)"
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = f"cuda:{local}"
+
+    sc = make_scene("c2")
+    scene = M.Scene(sc, device=local)
+    info = scene.info()
+    V = args.views
+    steps_total = args.warmup + args.steps
+    batches = [orbit_cameras(N_ORBIT, indices=views_for(rank, world, s, V)) for s in range(steps_total)]
+
+    stream = torch.cuda.Stream()
+    gstream = torch.cuda.Stream()
+    frames = [torch.empty((V, H_IMG, W_IMG, 4), dtype=torch.uint8, device=dev) for _ in range(2)]
+
+    # ---- counters pass over exactly the launches timed below (untimed, same views)
+    algo_bytes, n_eval, n_donly, n_skip, n_seg = [], 0, 0, 0, 0
+    with torch.cuda.stream(stream):
+        for s in range(args.warmup, steps_total):
+            st = M.merf_render(scene.handle, batches[s], W_IMG, H_IMG, frames[0], fmt=M.MERF_RGBA_U8,
+                               stream=stream, stats=True)
+            app = st["evaluated"] - st["density_only"]
+            algo_bytes.append(BYTES_APPEARANCE * app + BYTES_DENSITY_ONLY * st["density_only"]
+                              + BYTES_OUT * st["rays"])
+            n_eval += st["evaluated"]
+            n_donly += st["density_only"]
+            n_skip += st["skips"]
+            n_seg += st["segments"]
+    rays_per_step = V * W_IMG * H_IMG
+
+    def step(s):
+        buf = frames[s & 1]
+        with torch.cuda.stream(stream):
+            if world > 1:
+                stream.wait_stream(gstream)          # buffer reuse after its gather
+            ev0[s].record(stream)
+            M.merf_render(scene.handle, batches[s], W_IMG, H_IMG, buf, fmt=M.MERF_RGBA_U8, stream=stream)
+            ev1[s].record(stream)
+        if world > 1:
+            gstream.wait_stream(stream)
+            with torch.cuda.stream(gstream):
+                gather_frames(buf, rank, world)
+
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(steps_total)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(steps_total)]
+    for s in range(args.warmup):
+        step(s)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    t_start.record(stream)
+    for s in range(args.warmup, steps_total):
+        step(s)
+    stream.wait_stream(gstream)
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    if world > 1:
+        dist.barrier()
+    ms = t_start.elapsed_time(t_end)
+    kern_ms = [ev0[s].elapsed_time(ev1[s]) for s in range(args.warmup, steps_total)]
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    total_rays = rays_per_step * world * args.steps
+    value = total_rays / (ms / 1e3)
+
+    # ---- roofline of the dominant kernel (the fused render kernel, one launch per step)
+    peak, peak_src = _peaks()
+    avg_launch_ms = sum(kern_ms) / len(kern_ms)
+    bytes_per_launch = sum(algo_bytes) / len(algo_bytes)
+    achieved = bytes_per_launch / (avg_launch_ms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": _ncu_traffic(), "peak_source": peak_src,
+                "kernel": "merf::render_kernel<KF_U8>", "avg_launch_ms": avg_launch_ms,
+                "algorithmic_bytes_per_launch": bytes_per_launch,
+                "bytes_model": "160 B per evaluated sample with alpha > 0, 20 B per density-only "
+                               "sample, 4 B RGBA8 per ray (SURVEY 8(d))"}
+
+    # ---- end to end through the C ABI with host buffers (pinned), copies in the timed region
+    e2e = None
+    if not args.no_e2e:
+        host = torch.empty((V, H_IMG, W_IMG, 4), dtype=torch.uint8).pin_memory()
+        for s in range(min(2, args.warmup)):
+            M.merf_render_host(scene.handle, batches[s], W_IMG, H_IMG, host, fmt=M.MERF_RGBA_U8, stream=stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for s in range(args.warmup, steps_total):
+            M.merf_render_host(scene.handle, batches[s], W_IMG, H_IMG, host, fmt=M.MERF_RGBA_U8, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ems], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": total_rays / (ems / 1e3), "unit": "rays/s",
+               "h2d_bytes_per_step": V * 136, "d2h_bytes_per_step": V * W_IMG * H_IMG * 4,
+               "path": "merf_render_host (C ABI, pinned host output, render/copy overlapped in chunks of 4 views)"}
+
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu_baseline and world == 1:
+            cpu = cpu_baseline(sc, orbit_cameras(N_ORBIT, indices=[0])[0], sample_stride=2)
+        n_ray_timed = rays_per_step * args.steps
+        line = {
+            "metric": METRIC, "value": value, "unit": "rays/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "orbit1080p_paper_scale_merf",
+                       "views_per_rank_per_step": V, "W": W_IMG, "H": H_IMG,
+                       "scene": {k: info[k] for k in ("L", "R", "level_res", "n_blocks", "device_bytes")},
+                       "block_fraction": info["n_blocks"] / (info["L"] // 8) ** 3 if info["L"] else None,
+                       "l2": "no flush: inputs (scene %.0f MB) larger than the 126 MB L2; each step renders "
+                             "different orbit views" % (info["device_bytes"] / 1e6),
+                       "parallelism": f"views sharded over {world} rank(s), scene replicated, "
+                                      "NCCL frame gather to rank 0",
+                       "dtype_detail": "u8 features, fp64 ray setup/int64 lattice, fp32 shading"},
+            "fps": value / (W_IMG * H_IMG),
+            "fps_per_gpu": value / (W_IMG * H_IMG) / world,
+            "samples_per_sec": n_eval * world / (ms / 1e3),
+            "mean_evaluated_samples_per_ray": n_eval / n_ray_timed,
+            "density_only_fraction": n_donly / max(n_eval, 1),
+            "mean_skips_per_ray": n_skip / n_ray_timed,
+            "mean_segments_per_ray": n_seg / n_ray_timed,
+            "gather_gbs": achieved,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": args.steps * math.ceil(V / 16),
+            "clocks": clk,
+            "paper_context": PAPER_CONTEXT,
+        }
+        print(json.dumps(line), flush=True)
+    scene.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,251 @@
+/*
+ * merf.h -- C ABI of the B200-native MERF baked-scene renderer (libmerf.so).
+ *
+ * The library renders a baked MERF scene (Reiser et al., arXiv 2302.12249; "P:<n>" below is
+ * line n of the paper text /root/reference/PAPER.md) with hand-written sm_100a CUDA kernels:
+ * per ray, piecewise-projective contraction and region clipping (Sec. 4.2),
+ * hierarchical occupancy skipping in contracted space, block-sparse 3D grid +
+ * tri-plane gather of uint8 features, dequantised and summed (Eq. 5, Eq. 7
+ * P:254-258), decode (Eq. 6), front-to-back compositing with early termination
+ * (Eq. 1-2) and one deferred MLP per pixel (Eq. 3).
+ * Readings of the paper where it is silent (D1..D22) are listed in DESIGN.md.
+ *
+ * Conventions
+ *   - Plain C, no exceptions cross the ABI, nothing aborts.  Every call returns a
+ *     merf_status; on failure merf_last_error() returns a thread-local message.
+ *   - Host pointers are marked [host], device pointers [device].  Device pointers must be
+ *     allocations on the scene's device (e.g. torch tensors' data_ptr()).
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  Compute
+ *     calls are asynchronous on that stream unless documented otherwise.
+ *   - Ownership: inputs are caller-owned and only read; merf_scene_upload copies everything
+ *     it needs, so the caller may free its arrays after it returns.  The scene handle owns
+ *     all device memory it allocated until merf_scene_free.  Output buffers are caller-owned.
+ *   - Thread safety: a scene is immutable after upload; concurrent renders of one scene on
+ *     different streams are safe.  merf_scene_free must not race with renders.
+ *
+ * Layouts (all little-endian, C order)
+ *   occupancy bits : level of resolution N is N^3 bits, linear index (z*N + y)*N + x,
+ *                    packed LSB-first into uint32 words ((N^3 + 31) / 32 words).
+ *   planes         : uint8 [3][R][R][C]; plane 0 = P_x indexed [z][y], plane 1 = P_y [z][x],
+ *                    plane 2 = P_z [y][x].  Texel i is centred at
+ *                    -2 + (i + 1/2) * 4/R in contracted space (reading D9).
+ *   block_index    : int32 [(L/8)^3], slot (bz*nb + by)*nb + bx, -1 = block not stored.
+ *   atlas          : uint8 [n_blocks][9][9][9][C], (z,y,x): block data voxels 8b..8b+7 plus a
+ *                    1-voxel apron at 8b+8 (clamped to L-1) so trilinear corners never cross
+ *                    blocks (reading D11).
+ *   channels       : C = 8: [density, r, g, b, f0, f1, f2, f3] (reading D12); byte b
+ *                    decodes to 2m*b/255 - m with m = 14 (density) / 7 (others) (Eq. 7).
+ *   mlp            : float32 [883] = W0[16][34] b0[16] W1[16][16] b1[16] W2[3][16] b2[3];
+ *                    input [C_d(3), F(4), d(3), sin/cos(2^k d_j) j outer, k = 0..3 inner,
+ *                    sin before cos] (readings D16-D17).
+ *   camera         : merf_camera below; OpenCV pinhole, pixel centres (reading D18).
+ *   output         : MERF_RGB_F32 -> float [n_cams][H][W][3]; MERF_RGBA_U8 -> uint8
+ *                    [n_cams][H][W][4], round(255*C), alpha = 255.
+ */
+#ifndef MERF_H_
+#define MERF_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    MERF_OK = 0,
+    MERF_EINVAL = 1,     /* invalid argument (null pointer, bad size, bad descriptor)     */
+    MERF_ENOMEM = 2,     /* device allocation failed                                      */
+    MERF_ECUDA = 3,      /* a CUDA runtime call or kernel launch failed                   */
+    MERF_ENCCL = 4,      /* reserved (frame gather is done by the caller's process group) */
+    MERF_EMISMATCH = 5   /* scene arrays inconsistent (unsound block index, bad entries)  */
+} merf_status;
+
+enum { MERF_RGB_F32 = 0, MERF_RGBA_U8 = 1 };
+
+enum {
+    MERF_NO_EARLY_TERM = 1u,   /* disable termination at T < t_min                */
+    MERF_COUNTERS = 2u,        /* accumulate merf_stats (adds device atomics)             */
+    MERF_DENSE = 4u            /* debug: dense stepping gated by the finest level only     */
+};
+
+#define MERF_MAX_LEVELS 4
+#define MERF_FIXED_BITS 40     /* lattice fraction bits F (reading D8)                       */
+
+typedef struct {
+    int32_t L;                  /* 3D grid resolution: power of two >= 8, or 0 = no grid      */
+    int32_t R;                  /* plane resolution: power of two >= 2, or 0 = no planes      */
+    int32_t C;                  /* channels, must be 8                                        */
+    int32_t n_levels;           /* occupancy levels, 1..MERF_MAX_LEVELS                      */
+    int32_t level_res[MERF_MAX_LEVELS]; /* coarse -> fine, powers of two, each divides next;
+                                   the last (finest) level gates field evaluation  */
+    float m_density;            /* 14                                                 */
+    float m_appearance;         /* 7                                                 */
+    double step;                /* uniform contracted step Delta, power of two (D5)   */
+    float t_min;                /* termination transmittance, 2e-4                   */
+    float alpha_skip;           /* appearance read iff alpha > alpha_skip, 0 (D14)     */
+    uint32_t source_mask;       /* bit0 V, bit1 P_x, bit2 P_y, bit3 P_z (config-5 variants)  */
+} merf_scene_desc;
+
+typedef struct {
+    double c2w[12];             /* camera-to-world, row-major 3x4 [R | t]; OpenCV axes       */
+    double fx, fy, cx, cy;      /* pinhole intrinsics in pixels                              */
+    double t_near;              /* ray start parameter, >= 0                                 */
+} merf_camera;
+
+typedef struct {
+    int64_t rays;
+    int64_t segments;           /* kept contracted segments (<= 7 per ray)                    */
+    int64_t evaluated;          /* samples whose finest occupancy bit is set (field read)    */
+    int64_t density_only;       /* evaluated samples with alpha <= alpha_skip (20 B read)     */
+    int64_t skips;              /* empty-cell jumps                                   */
+    int64_t missing_blocks;     /* evaluated samples whose V block is absent (must be 0)      */
+    int64_t region_segments[7]; /* kept segments per region (core, +x, -x, +y, -y, +z, -z)   */
+} merf_stats;
+
+typedef struct {
+    int32_t L, R, C, n_levels;
+    int32_t level_res[MERF_MAX_LEVELS];
+    int64_t n_blocks;
+    int64_t canonical_blocks;   /* blocks the canonical allocation needs (<= n_blocks)        */
+    int64_t device_bytes;       /* device memory owned by the scene                           */
+    int32_t device;
+} merf_scene_info;
+
+typedef struct merf_scene merf_scene;
+
+/* Thread-local description of the last failure ("" if none). */
+const char *merf_last_error(void);
+
+/* Library/ABI version (major*10000 + minor*100 + patch). */
+int32_t merf_version(void);
+
+/*
+ * Copy a baked scene to `device` and build its acceleration structures:
+ * the coarser occupancy levels by max-pooling the finest and the canonical
+ * block allocation (reading D11).
+ *   desc        [host] scene descriptor (validated: L, R powers of two, C == 8, levels
+ *               powers of two dividing each other, step a power of two > 0).
+ *   planes      [host] uint8 [3][R][R][C] (ignored if R == 0).
+ *   block_index [host] int32 [(L/8)^3] or NULL: NULL means "atlas is in canonical order"
+ *               and requires n_blocks == the canonical count.  A non-NULL index is checked:
+ *               entries in [-1, n_blocks) and every canonically needed block stored
+ *               (soundness: every evaluated sample has its block), else MERF_EMISMATCH.
+ *   atlas       [host] uint8 [n_blocks][9][9][9][C] (ignored if L == 0).
+ *   occ_finest  [host] uint32 bits of the finest level (level_res[n_levels-1]).
+ *   mlp         [host] float [883].
+ *   out         [host] receives the handle.
+ * Synchronous.  Errors: MERF_EINVAL, MERF_ENOMEM, MERF_ECUDA, MERF_EMISMATCH.
+ */
+merf_status merf_scene_upload(const merf_scene_desc *desc, const uint8_t *planes,
+                              const int32_t *block_index, const uint8_t *atlas, int64_t n_blocks,
+                              const uint32_t *occ_finest, const float *mlp, int32_t device,
+                              merf_scene **out);
+
+/* Release the scene's device memory (synchronises its device).  NULL is a no-op. */
+merf_status merf_scene_free(merf_scene *scene);
+
+/* Scene facts (host struct). */
+merf_status merf_scene_info_get(const merf_scene *scene, merf_scene_info *info);
+
+/* Device copy of occupancy level `level` (0 = coarsest) into `bits_out` [device]
+ * ((N^3+31)/32 words), asynchronous on `stream`. */
+merf_status merf_scene_occupancy(const merf_scene *scene, int32_t level, uint32_t *bits_out,
+                                 void *stream);
+
+/* Device copy of the scene's block index [(L/8)^3] int32 into `index_out` [device]. */
+merf_status merf_scene_block_index(const merf_scene *scene, int32_t *index_out, void *stream);
+
+/*
+ * Render n_cams full frames of W x H pixels (the hot path, Sec. 6).
+ *   cams   [host] n_cams cameras (copied into the launch; the caller may reuse them).
+ *   format MERF_RGB_F32 or MERF_RGBA_U8; out [device] caller-owned output (see Layouts).
+ *   flags  MERF_NO_EARLY_TERM | MERF_COUNTERS | MERF_DENSE.
+ *   stats  [host] optional; if non-NULL the call enables counters, synchronises `stream`
+ *          and fills *stats (so it is no longer asynchronous).
+ * Errors: MERF_EINVAL (null, W/H/n_cams <= 0, W*H*n_cams > 2^31, bad format), MERF_ECUDA.
+ */
+merf_status merf_render(const merf_scene *scene, const merf_camera *cams, int32_t n_cams,
+                        int32_t W, int32_t H, int32_t format, void *out, uint32_t flags,
+                        void *stream, merf_stats *stats);
+
+/*
+ * End-to-end variant with HOST output: renders into scene-owned device staging buffers in
+ * chunks and copies each finished chunk to `out_host` [host] (pinned memory recommended)
+ * while the next chunk renders.  Synchronous on return.  Same layouts/errors as merf_render.
+ */
+merf_status merf_render_host(const merf_scene *scene, const merf_camera *cams, int32_t n_cams,
+                             int32_t W, int32_t H, int32_t format, void *out_host,
+                             uint32_t flags, void *stream);
+
+/*
+ * Render explicit rays: o, d [device] double [n][3] (d unit length), t_near [device] double [n]
+ * or NULL (0).  rgb [device] float [n][3].  Errors: MERF_EINVAL, MERF_ECUDA.
+ */
+merf_status merf_render_rays(const merf_scene *scene, const double *o, const double *d,
+                             const double *t_near, int64_t n, float *rgb, uint32_t flags,
+                             void *stream, merf_stats *stats);
+
+/*
+ * Per-ray visited-cell trace (debug/parity) for pixels `pixel_ids` [device] int64 [n]
+ * (id = j*W + i) of camera `cam` [host].  For each evaluated sample, in march order:
+ *   cells_out [device] uint64 [n][max_per_ray]: (segment ordinal << 61) | (k << 40) | cell,
+ *             cell = finest-level linear index (z*N + y)*N + x;
+ *   T_out     [device] float [n][max_per_ray]: transmittance after the sample (may be NULL);
+ *   counts_out[device] int32 [n]: number of evaluated samples (may exceed max_per_ray; only
+ *             the first max_per_ray are stored).
+ * Errors: MERF_EINVAL, MERF_ECUDA.
+ */
+merf_status merf_trace(const merf_scene *scene, const merf_camera *cam, int32_t W,
+                       const int64_t *pixel_ids, int64_t n, int32_t max_per_ray,
+                       uint64_t *cells_out, float *T_out, int32_t *counts_out, uint32_t flags,
+                       void *stream);
+
+/* One contracted segment of a ray: world interval [t_a, t_b] (t_b = +inf for the
+ * unbounded last one), region (0 core, 1 + 2j + (s < 0)), lattice origin Qa = llrint(c_a 2^40),
+ * lattice step U = llrint(u Delta 2^40) and sample count K = ceil(l / Delta) (readings D5-D8). */
+typedef struct {
+    double t_a, t_b;
+    int64_t Qa[3];
+    int64_t U[3];
+    int32_t K;
+    int32_t region;
+} merf_segment;
+
+/*
+ * Per-ray contracted segments (debug/parity of the clipping step) for pixels `pixel_ids`
+ * [device] int64 [n] of camera `cam` [host]: segs_out [device] merf_segment [n][max_seg]
+ * (kept segments in order, zero-length ones dropped), counts_out [device] int32 [n].
+ * Errors: MERF_EINVAL, MERF_ECUDA.
+ */
+merf_status merf_segments(const merf_scene *scene, const merf_camera *cam, int32_t W,
+                          const int64_t *pixel_ids, int64_t n, int32_t max_seg,
+                          merf_segment *segs_out, int32_t *counts_out, void *stream);
+
+/*
+ * contract_pi of n points: x, y [device] double [n][3]; region [device] int32 [n]
+ * or NULL (0 = core, 1 + 2j + (x_j < 0) for the outer region of axis j, reading D1-D2).
+ */
+merf_status merf_contract(const double *x, int64_t n, double *y, int32_t *region, void *stream);
+
+/*
+ * Occupancy pyramid (K0): max-pool the finest level `finest_bits` [device] into every
+ * coarser level of `desc`, written coarse -> fine, concatenated, to `levels_out` [device]
+ * (sum over levels 0..n_levels-2 of (N^3+31)/32 words).  Asynchronous.
+ */
+merf_status merf_build_occupancy(const uint32_t *finest_bits, const merf_scene_desc *desc,
+                                 uint32_t *levels_out, void *stream);
+
+/*
+ * Canonical block allocation (K1, reading D11): a block slot is needed iff some occupied
+ * finest cell can produce a sample whose trilinear base voxel lies in it; needed slots are
+ * numbered in raster order.  finest_bits [device]; index_out [device] int32 [(L/8)^3];
+ * n_blocks [host] receives the count.  Synchronises `stream`.
+ */
+merf_status merf_build_block_index(const uint32_t *finest_bits, const merf_scene_desc *desc,
+                                   int32_t *index_out, int64_t *n_blocks, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MERF_H_ */

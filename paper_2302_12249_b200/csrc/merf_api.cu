@@ -1,0 +1,492 @@
+// merf_api.cu -- the C ABI of libmerf (include/merf.h): validation, device memory, launch
+// plumbing.  No compute happens here; every step of the path runs in the kernels of
+// merf_render.cu / merf_build.cu.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/merf.h"
+#include "merf_device.cuh"
+#include "merf_kernels.h"
+
+using namespace merf;
+
+struct merf_scene {
+    merf_scene_desc desc;
+    DevScene dev;
+    int device;
+    int64_t n_blocks;
+    int64_t canonical_blocks;
+    int64_t device_bytes;
+    std::vector<void*> allocs;
+    // staging for merf_render_host (lazily allocated, guarded by the caller's usage)
+    void* stage[2] = {nullptr, nullptr};
+    size_t stage_bytes = 0;
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+};
+
+static thread_local std::string g_err;
+
+static merf_status fail(merf_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+#define CUDA_TRY(expr)                                                                    \
+    do {                                                                                  \
+        cudaError_t _e = (expr);                                                          \
+        if (_e != cudaSuccess)                                                            \
+            return fail(_e == cudaErrorMemoryAllocation ? MERF_ENOMEM : MERF_ECUDA,       \
+                        "%s: %s (%s:%d)", #expr, cudaGetErrorString(_e), __FILE__, __LINE__); \
+    } while (0)
+
+static bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
+static int ilog2i(int64_t v) { int n = 0; while ((int64_t(1) << n) < v) n++; return n; }
+static int64_t occ_words(int N) { return ((int64_t)N * N * N + 31) / 32; }
+
+extern "C" const char* merf_last_error(void) { return g_err.c_str(); }
+extern "C" int32_t merf_version(void) { return 100; }
+
+static merf_status validate_desc(const merf_scene_desc* d) {
+    if (!d) return fail(MERF_EINVAL, "desc is NULL");
+    if (d->C != 8) return fail(MERF_EINVAL, "C must be 8 (got %d)", d->C);
+    if (d->L != 0 && (!is_pow2(d->L) || d->L < 8))
+        return fail(MERF_EINVAL, "L must be 0 or a power of two >= 8 (got %d)", d->L);
+    if (d->R != 0 && (!is_pow2(d->R) || d->R < 2))
+        return fail(MERF_EINVAL, "R must be 0 or a power of two >= 2 (got %d)", d->R);
+    if (d->L == 0 && d->R == 0) return fail(MERF_EINVAL, "scene has neither grid nor planes");
+    if (d->L > 4096 || d->R > 65536) return fail(MERF_EINVAL, "L or R too large");
+    if (d->n_levels < 1 || d->n_levels > MERF_MAX_LEVELS)
+        return fail(MERF_EINVAL, "n_levels must be in [1, %d]", MERF_MAX_LEVELS);
+    for (int i = 0; i < d->n_levels; i++) {
+        int N = d->level_res[i];
+        if (!is_pow2(N) || N > 2048) return fail(MERF_EINVAL, "level_res[%d] = %d not a power of two <= 2048", i, N);
+        if (i > 0 && (N % d->level_res[i - 1]) != 0)
+            return fail(MERF_EINVAL, "level_res[%d] does not divide level_res[%d]", i - 1, i);
+    }
+    if (!(d->step > 0.0)) return fail(MERF_EINVAL, "step must be > 0");
+    int e;
+    double m = frexp(d->step, &e);
+    if (m != 0.5 || d->step > 1.0 || d->step < 1e-6)
+        return fail(MERF_EINVAL, "step must be a power of two in [2^-19, 1] (got %g)", d->step);
+    if (!(d->t_min >= 0.f && d->t_min < 1.f)) return fail(MERF_EINVAL, "t_min must be in [0, 1)");
+    if (!(d->m_density > 0.f && d->m_appearance > 0.f)) return fail(MERF_EINVAL, "m must be > 0");
+    return MERF_OK;
+}
+
+static void fill_dev(merf_scene* s) {
+    const merf_scene_desc& d = s->desc;
+    DevScene& S = s->dev;
+    S.L = (d.source_mask & 1u) ? d.L : 0;
+    S.R = (d.source_mask & 14u) ? d.R : 0;
+    S.nb = S.L / 8;
+    S.n_levels = d.n_levels;
+    for (int i = 0; i < MERF_MAX_LEVELS; i++) {
+        S.level_res[i] = i < d.n_levels ? d.level_res[i] : 1;
+        S.level_shift[i] = kF + 2 - ilog2i(S.level_res[i]);
+    }
+    S.sV = S.L ? kF + 2 - ilog2i(S.L) : 0;
+    S.sP = S.R ? kF + 2 - ilog2i(S.R) : 0;
+    S.kd = (float)(2.0 * d.m_density / 255.0);
+    S.ka = (float)(2.0 * d.m_appearance / 255.0);
+    S.md = d.m_density;
+    S.ma = d.m_appearance;
+    S.use_v = S.L > 0;
+    for (int a = 0; a < 3; a++) S.use_p[a] = S.R > 0 && ((d.source_mask >> (1 + a)) & 1u);
+    S.n_src = S.use_v + S.use_p[0] + S.use_p[1] + S.use_p[2];
+    S.step = d.step;
+    S.lattice_step = d.step * (double)kOne;
+    S.step_f = (float)d.step;
+    S.t_min = d.t_min;
+    S.alpha_skip = d.alpha_skip;
+}
+
+template <typename T>
+static merf_status dalloc(merf_scene* s, T** p, size_t bytes) {
+    void* q = nullptr;
+    if (bytes == 0) bytes = 16;
+    cudaError_t e = cudaMalloc(&q, bytes);
+    if (e != cudaSuccess) return fail(MERF_ENOMEM, "cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e));
+    s->allocs.push_back(q);
+    s->device_bytes += (int64_t)bytes;
+    *p = reinterpret_cast<T*>(q);
+    return MERF_OK;
+}
+
+extern "C" merf_status merf_scene_free(merf_scene* s) {
+    if (!s) return MERF_OK;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(s->device);
+    cudaDeviceSynchronize();
+    for (void* p : s->allocs) cudaFree(p);
+    for (int i = 0; i < 2; i++) {
+        if (s->stage[i]) cudaFree(s->stage[i]);
+        if (s->ev[i]) cudaEventDestroy(s->ev[i]);
+    }
+    if (s->copy_stream) cudaStreamDestroy(s->copy_stream);
+    cudaSetDevice(prev);
+    delete s;
+    return MERF_OK;
+}
+
+extern "C" merf_status merf_scene_upload(const merf_scene_desc* desc, const uint8_t* planes,
+                                         const int32_t* block_index, const uint8_t* atlas,
+                                         int64_t n_blocks, const uint32_t* occ_finest,
+                                         const float* mlp, int32_t device, merf_scene** out) {
+    merf_status st = validate_desc(desc);
+    if (st) return st;
+    if (!out || !occ_finest || !mlp) return fail(MERF_EINVAL, "NULL out/occ_finest/mlp");
+    const bool use_v = desc->L > 0 && (desc->source_mask & 1u);
+    const bool use_p = desc->R > 0 && (desc->source_mask & 14u);
+    if (!use_v && !use_p) return fail(MERF_EINVAL, "source_mask selects no stored source");
+    if (use_p && !planes) return fail(MERF_EINVAL, "planes is NULL");
+    if (use_v && (!atlas || n_blocks < 0)) return fail(MERF_EINVAL, "atlas is NULL or n_blocks < 0");
+    if (use_v && n_blocks > (int64_t)INT32_MAX) return fail(MERF_EINVAL, "n_blocks too large");
+    int ndev = 0;
+    CUDA_TRY(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(MERF_EINVAL, "device %d out of range", device);
+    int prev = 0;
+    cudaGetDevice(&prev);
+    CUDA_TRY(cudaSetDevice(device));
+
+    merf_scene* s = new merf_scene();
+    s->desc = *desc;
+    s->device = device;
+    s->n_blocks = use_v ? n_blocks : 0;
+    fill_dev(s);
+    DevScene& S = s->dev;
+    auto bail = [&](merf_status e) { merf_scene_free(s); cudaSetDevice(prev); return e; };
+#define UP_TRY(expr) do { merf_status _s = (expr); if (_s) return bail(_s); } while (0)
+#define UPC_TRY(expr) do { cudaError_t _e = (expr); if (_e != cudaSuccess) \
+        return bail(fail(_e == cudaErrorMemoryAllocation ? MERF_ENOMEM : MERF_ECUDA, "%s: %s", #expr, cudaGetErrorString(_e))); } while (0)
+
+    cudaStream_t cs;
+    UPC_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    // ---- MLP weights
+    float* d_mlp;
+    UP_TRY(dalloc(s, &d_mlp, kMlpFloats * sizeof(float)));
+    UPC_TRY(cudaMemcpy(d_mlp, mlp, kMlpFloats * sizeof(float), cudaMemcpyHostToDevice));
+    S.mlp = d_mlp;
+    // ---- planes
+    if (use_p) {
+        size_t pb = (size_t)3 * desc->R * desc->R * 8;
+        uint8_t* d_pl;
+        UP_TRY(dalloc(s, &d_pl, pb));
+        UPC_TRY(cudaMemcpy(d_pl, planes, pb, cudaMemcpyHostToDevice));
+        S.planes = d_pl;
+    }
+    // ---- occupancy pyramid (K0)
+    const int nl = desc->n_levels;
+    const int Nf = desc->level_res[nl - 1];
+    uint32_t* d_occ[MERF_MAX_LEVELS] = {nullptr, nullptr, nullptr, nullptr};
+    for (int i = 0; i < nl; i++) UP_TRY(dalloc(s, &d_occ[i], occ_words(desc->level_res[i]) * 4));
+    UPC_TRY(cudaMemcpy(d_occ[nl - 1], occ_finest, occ_words(Nf) * 4, cudaMemcpyHostToDevice));
+    for (int i = 0; i < nl - 1; i++)
+        UPC_TRY(launch_maxpool_bits(d_occ[nl - 1], Nf, d_occ[i], desc->level_res[i], cs));
+    for (int i = 0; i < MERF_MAX_LEVELS; i++) S.occ[i] = d_occ[i < nl ? i : nl - 1];
+    // ---- block index (K1) + atlas
+    if (use_v) {
+        const int64_t slots = (int64_t)(desc->L / 8) * (desc->L / 8) * (desc->L / 8);
+        uint8_t* d_need;
+        int32_t* d_idx;
+        int32_t* d_scan;
+        int64_t* d_count;
+        unsigned long long* d_bad;
+        UPC_TRY(cudaMalloc(&d_need, slots));
+        UPC_TRY(cudaMalloc(&d_scan, slots * 8));
+        UPC_TRY(cudaMalloc(&d_count, 16));
+        UPC_TRY(cudaMalloc(&d_bad, 16));
+        UP_TRY(dalloc(s, &d_idx, slots * 4));
+        size_t tb = 0;
+        UPC_TRY(launch_block_number(nullptr, slots, nullptr, nullptr, nullptr, &tb, nullptr, cs));
+        void* d_tmp;
+        UPC_TRY(cudaMalloc(&d_tmp, tb + 16));
+        UPC_TRY(launch_block_need(d_occ[nl - 1], Nf, desc->L, d_need, cs));
+        int64_t canon = 0;
+        if (block_index) {
+            UPC_TRY(cudaMemcpy(d_idx, block_index, slots * 4, cudaMemcpyHostToDevice));
+            int32_t* d_canon;
+            UPC_TRY(cudaMalloc(&d_canon, slots * 4));
+            UPC_TRY(launch_block_number(d_need, slots, d_canon, d_count, d_tmp, &tb, d_scan, cs));
+            UPC_TRY(cudaStreamSynchronize(cs));
+            cudaFree(d_canon);
+        } else {
+            UPC_TRY(launch_block_number(d_need, slots, d_idx, d_count, d_tmp, &tb, d_scan, cs));
+        }
+        UPC_TRY(cudaMemsetAsync(d_bad, 0, 8, cs));
+        UPC_TRY(launch_block_check(d_need, d_idx, slots, n_blocks, d_bad, cs));
+        unsigned long long bad = 0;
+        UPC_TRY(cudaMemcpyAsync(&canon, d_count, 8, cudaMemcpyDeviceToHost, cs));
+        UPC_TRY(cudaMemcpyAsync(&bad, d_bad, 8, cudaMemcpyDeviceToHost, cs));
+        UPC_TRY(cudaStreamSynchronize(cs));
+        cudaFree(d_need); cudaFree(d_scan); cudaFree(d_count); cudaFree(d_bad); cudaFree(d_tmp);
+        s->canonical_blocks = canon;
+        if (!block_index && canon != n_blocks)
+            return bail(fail(MERF_EMISMATCH, "canonical allocation needs %lld blocks, atlas has %lld",
+                             (long long)canon, (long long)n_blocks));
+        if (bad)
+            return bail(fail(MERF_EMISMATCH, "block index unsound or out of range at %llu slots "
+                                             "(an occupied cell's block is missing)", bad));
+        size_t ab = (size_t)n_blocks * 729 * 8;
+        uint8_t* d_at;
+        UP_TRY(dalloc(s, &d_at, ab));
+        if (ab) UPC_TRY(cudaMemcpy(d_at, atlas, ab, cudaMemcpyHostToDevice));
+        S.block_index = d_idx;
+        S.atlas = d_at;
+    }
+    UPC_TRY(cudaStreamSynchronize(cs));
+    cudaStreamDestroy(cs);
+    cudaSetDevice(prev);
+    *out = s;
+    return MERF_OK;
+#undef UP_TRY
+#undef UPC_TRY
+}
+
+extern "C" merf_status merf_scene_info_get(const merf_scene* s, merf_scene_info* info) {
+    if (!s || !info) return fail(MERF_EINVAL, "NULL argument");
+    memset(info, 0, sizeof(*info));
+    info->L = s->dev.L;
+    info->R = s->dev.R;
+    info->C = 8;
+    info->n_levels = s->desc.n_levels;
+    for (int i = 0; i < MERF_MAX_LEVELS; i++) info->level_res[i] = s->desc.level_res[i];
+    info->n_blocks = s->n_blocks;
+    info->canonical_blocks = s->canonical_blocks;
+    info->device_bytes = s->device_bytes;
+    info->device = s->device;
+    return MERF_OK;
+}
+
+extern "C" merf_status merf_scene_occupancy(const merf_scene* s, int32_t level, uint32_t* bits_out,
+                                            void* stream) {
+    if (!s || !bits_out) return fail(MERF_EINVAL, "NULL argument");
+    if (level < 0 || level >= s->desc.n_levels) return fail(MERF_EINVAL, "level out of range");
+    CUDA_TRY(cudaMemcpyAsync(bits_out, s->dev.occ[level], occ_words(s->desc.level_res[level]) * 4,
+                             cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    return MERF_OK;
+}
+
+extern "C" merf_status merf_scene_block_index(const merf_scene* s, int32_t* index_out, void* stream) {
+    if (!s || !index_out) return fail(MERF_EINVAL, "NULL argument");
+    if (!s->dev.L) return fail(MERF_EINVAL, "scene has no 3D grid");
+    int64_t slots = (int64_t)s->dev.nb * s->dev.nb * s->dev.nb;
+    CUDA_TRY(cudaMemcpyAsync(index_out, s->dev.block_index, slots * 4, cudaMemcpyDeviceToDevice,
+                             (cudaStream_t)stream));
+    return MERF_OK;
+}
+
+static merf_status check_frames(const merf_scene* s, const merf_camera* cams, int32_t n_cams,
+                                int32_t W, int32_t H, int32_t format, const void* out) {
+    if (!s || !cams || !out) return fail(MERF_EINVAL, "NULL scene/cams/out");
+    if (n_cams <= 0 || W <= 0 || H <= 0) return fail(MERF_EINVAL, "n_cams, W, H must be > 0");
+    if ((int64_t)W * H * n_cams > ((int64_t)1 << 31)) return fail(MERF_EINVAL, "W*H*n_cams too large");
+    if (H > 65535 * 8) return fail(MERF_EINVAL, "H too large");
+    if (format != MERF_RGB_F32 && format != MERF_RGBA_U8) return fail(MERF_EINVAL, "bad format %d", format);
+    for (int i = 0; i < n_cams; i++)
+        if (!(cams[i].fx > 0 && cams[i].fy > 0 && cams[i].t_near >= 0))
+            return fail(MERF_EINVAL, "camera %d: fx, fy must be > 0 and t_near >= 0", i);
+    return MERF_OK;
+}
+
+static void to_stats(const unsigned long long* h, merf_stats* st) {
+    st->rays = (int64_t)h[0];
+    st->segments = (int64_t)h[1];
+    st->evaluated = (int64_t)h[2];
+    st->density_only = (int64_t)h[3];
+    st->skips = (int64_t)h[4];
+    st->missing_blocks = (int64_t)h[5];
+    for (int g = 0; g < 7; g++) st->region_segments[g] = (int64_t)h[6 + g];
+}
+
+static merf_status render_frames(const merf_scene* s, const merf_camera* cams, int32_t n_cams,
+                                 int32_t W, int32_t H, int32_t format, void* out, uint32_t flags,
+                                 cudaStream_t st, unsigned long long* d_stats) {
+    const size_t px_bytes = format == MERF_RGBA_U8 ? 4 : 12;
+    for (int c0 = 0; c0 < n_cams; c0 += kMaxCams) {
+        CamBatch cb;
+        cb.n = n_cams - c0 < kMaxCams ? n_cams - c0 : kMaxCams;
+        for (int i = 0; i < cb.n; i++) cb.cam[i] = cams[c0 + i];
+        void* o = (char*)out + (size_t)c0 * W * H * px_bytes;
+        CUDA_TRY(launch_render_frames(s->dev, cb, W, H, format, o, flags, d_stats, st));
+    }
+    return MERF_OK;
+}
+
+extern "C" merf_status merf_render(const merf_scene* s, const merf_camera* cams, int32_t n_cams,
+                                   int32_t W, int32_t H, int32_t format, void* out, uint32_t flags,
+                                   void* stream, merf_stats* stats) {
+    merf_status e = check_frames(s, cams, n_cams, W, H, format, out);
+    if (e) return e;
+    cudaStream_t st = (cudaStream_t)stream;
+    unsigned long long* d_stats = nullptr;
+    if (stats || (flags & MERF_COUNTERS)) {
+        CUDA_TRY(cudaMallocAsync(&d_stats, 16 * sizeof(unsigned long long), st));
+        CUDA_TRY(cudaMemsetAsync(d_stats, 0, 16 * sizeof(unsigned long long), st));
+    }
+    e = render_frames(s, cams, n_cams, W, H, format, out, flags, st, d_stats);
+    if (e) return e;
+    if (d_stats) {
+        unsigned long long h[16];
+        CUDA_TRY(cudaMemcpyAsync(h, d_stats, sizeof(h), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaFreeAsync(d_stats, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        if (stats) to_stats(h, stats);
+    }
+    return MERF_OK;
+}
+
+extern "C" merf_status merf_render_host(const merf_scene* cs, const merf_camera* cams, int32_t n_cams,
+                                        int32_t W, int32_t H, int32_t format, void* out_host,
+                                        uint32_t flags, void* stream) {
+    merf_status e = check_frames(cs, cams, n_cams, W, H, format, out_host);
+    if (e) return e;
+    merf_scene* s = const_cast<merf_scene*>(cs);
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t px_bytes = format == MERF_RGBA_U8 ? 4 : 12;
+    const size_t frame = (size_t)W * H * px_bytes;
+    const int chunk = 4;   // views per chunk; chunk i+1 renders while chunk i copies out
+    const size_t need = frame * chunk;
+    if (s->stage_bytes < need) {
+        for (int i = 0; i < 2; i++) {
+            if (s->stage[i]) cudaFree(s->stage[i]);
+            s->stage[i] = nullptr;
+        }
+        s->stage_bytes = 0;
+        for (int i = 0; i < 2; i++) CUDA_TRY(cudaMalloc(&s->stage[i], need));
+        s->stage_bytes = need;
+    }
+    if (!s->copy_stream) CUDA_TRY(cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; i++)
+        if (!s->ev[i]) CUDA_TRY(cudaEventCreateWithFlags(&s->ev[i], cudaEventDisableTiming));
+    cudaEvent_t copied[2];
+    for (int i = 0; i < 2; i++) CUDA_TRY(cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming));
+    bool pending[2] = {false, false};
+    int b = 0;
+    for (int c0 = 0; c0 < n_cams; c0 += chunk, b ^= 1) {
+        int n = n_cams - c0 < chunk ? n_cams - c0 : chunk;
+        if (pending[b]) CUDA_TRY(cudaStreamWaitEvent(st, copied[b], 0));   // buffer free again
+        e = render_frames(s, cams + c0, n, W, H, format, s->stage[b], flags, st, nullptr);
+        if (e) return e;
+        CUDA_TRY(cudaEventRecord(s->ev[b], st));
+        CUDA_TRY(cudaStreamWaitEvent(s->copy_stream, s->ev[b], 0));
+        CUDA_TRY(cudaMemcpyAsync((char*)out_host + (size_t)c0 * frame, s->stage[b], frame * n,
+                                 cudaMemcpyDeviceToHost, s->copy_stream));
+        CUDA_TRY(cudaEventRecord(copied[b], s->copy_stream));
+        pending[b] = true;
+    }
+    CUDA_TRY(cudaStreamSynchronize(s->copy_stream));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    for (int i = 0; i < 2; i++) cudaEventDestroy(copied[i]);
+    return MERF_OK;
+}
+
+extern "C" merf_status merf_render_rays(const merf_scene* s, const double* o, const double* d,
+                                        const double* t_near, int64_t n, float* rgb, uint32_t flags,
+                                        void* stream, merf_stats* stats) {
+    if (!s || !o || !d || !rgb) return fail(MERF_EINVAL, "NULL argument");
+    if (n < 0 || n > ((int64_t)1 << 31)) return fail(MERF_EINVAL, "bad ray count");
+    if (n == 0) return MERF_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    unsigned long long* d_stats = nullptr;
+    if (stats) {
+        CUDA_TRY(cudaMallocAsync(&d_stats, 16 * sizeof(unsigned long long), st));
+        CUDA_TRY(cudaMemsetAsync(d_stats, 0, 16 * sizeof(unsigned long long), st));
+    }
+    CUDA_TRY(launch_render_rays(s->dev, o, d, t_near, n, rgb, flags, d_stats, st));
+    if (d_stats) {
+        unsigned long long h[16];
+        CUDA_TRY(cudaMemcpyAsync(h, d_stats, sizeof(h), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaFreeAsync(d_stats, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        to_stats(h, stats);
+    }
+    return MERF_OK;
+}
+
+extern "C" merf_status merf_trace(const merf_scene* s, const merf_camera* cam, int32_t W,
+                                  const int64_t* pixel_ids, int64_t n, int32_t max_per_ray,
+                                  uint64_t* cells_out, float* T_out, int32_t* counts_out,
+                                  uint32_t flags, void* stream) {
+    if (!s || !cam || !pixel_ids || !cells_out || !counts_out) return fail(MERF_EINVAL, "NULL argument");
+    if (n < 0 || n > ((int64_t)1 << 31) || W <= 0 || max_per_ray < 0)
+        return fail(MERF_EINVAL, "bad n / W / max_per_ray");
+    if (!(cam->fx > 0 && cam->fy > 0 && cam->t_near >= 0)) return fail(MERF_EINVAL, "bad camera");
+    if (n == 0) return MERF_OK;
+    CUDA_TRY(launch_trace(s->dev, *cam, W, pixel_ids, n, max_per_ray, cells_out, T_out, counts_out,
+                          flags, (cudaStream_t)stream));
+    return MERF_OK;
+}
+
+extern "C" merf_status merf_segments(const merf_scene* s, const merf_camera* cam, int32_t W,
+                                     const int64_t* pixel_ids, int64_t n, int32_t max_seg,
+                                     merf_segment* segs_out, int32_t* counts_out, void* stream) {
+    if (!s || !cam || !pixel_ids || !segs_out || !counts_out) return fail(MERF_EINVAL, "NULL argument");
+    if (n < 0 || n > ((int64_t)1 << 31) || W <= 0 || max_seg < 0) return fail(MERF_EINVAL, "bad n / W / max_seg");
+    if (!(cam->fx > 0 && cam->fy > 0 && cam->t_near >= 0)) return fail(MERF_EINVAL, "bad camera");
+    if (n == 0) return MERF_OK;
+    CUDA_TRY(launch_segments(s->dev, *cam, W, pixel_ids, n, max_seg, segs_out, counts_out,
+                             (cudaStream_t)stream));
+    return MERF_OK;
+}
+
+extern "C" merf_status merf_contract(const double* x, int64_t n, double* y, int32_t* region, void* stream) {
+    if (n < 0) return fail(MERF_EINVAL, "n < 0");
+    if (n > 0 && (!x || !y)) return fail(MERF_EINVAL, "NULL argument");
+    CUDA_TRY(launch_contract(x, n, y, region, (cudaStream_t)stream));
+    return MERF_OK;
+}
+
+extern "C" merf_status merf_build_occupancy(const uint32_t* finest_bits, const merf_scene_desc* desc,
+                                            uint32_t* levels_out, void* stream) {
+    merf_status e = validate_desc(desc);
+    if (e) return e;
+    if (!finest_bits || (!levels_out && desc->n_levels > 1)) return fail(MERF_EINVAL, "NULL argument");
+    const int nl = desc->n_levels, Nf = desc->level_res[nl - 1];
+    uint32_t* o = levels_out;
+    for (int i = 0; i < nl - 1; i++) {
+        CUDA_TRY(launch_maxpool_bits(finest_bits, Nf, o, desc->level_res[i], (cudaStream_t)stream));
+        o += occ_words(desc->level_res[i]);
+    }
+    return MERF_OK;
+}
+
+extern "C" merf_status merf_build_block_index(const uint32_t* finest_bits, const merf_scene_desc* desc,
+                                              int32_t* index_out, int64_t* n_blocks, void* stream) {
+    merf_status e = validate_desc(desc);
+    if (e) return e;
+    if (!finest_bits || !index_out || !n_blocks) return fail(MERF_EINVAL, "NULL argument");
+    if (desc->L <= 0) return fail(MERF_EINVAL, "L must be > 0");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t slots = (int64_t)(desc->L / 8) * (desc->L / 8) * (desc->L / 8);
+    const int Nf = desc->level_res[desc->n_levels - 1];
+    uint8_t* d_need = nullptr;
+    int32_t* d_scan = nullptr;
+    int64_t* d_count = nullptr;
+    void* d_tmp = nullptr;
+    size_t tb = 0;
+    CUDA_TRY(launch_block_number(nullptr, slots, nullptr, nullptr, nullptr, &tb, nullptr, st));
+    CUDA_TRY(cudaMalloc(&d_need, slots));
+    CUDA_TRY(cudaMalloc(&d_scan, slots * 8));
+    CUDA_TRY(cudaMalloc(&d_count, 16));
+    CUDA_TRY(cudaMalloc(&d_tmp, tb + 16));
+    CUDA_TRY(launch_block_need(finest_bits, Nf, desc->L, d_need, st));
+    CUDA_TRY(launch_block_number(d_need, slots, index_out, d_count, d_tmp, &tb, d_scan, st));
+    int64_t cnt = 0;
+    CUDA_TRY(cudaMemcpyAsync(&cnt, d_count, 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    cudaFree(d_need); cudaFree(d_scan); cudaFree(d_count); cudaFree(d_tmp);
+    *n_blocks = cnt;
+    return MERF_OK;
+}

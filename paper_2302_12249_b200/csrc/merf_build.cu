@@ -1,0 +1,166 @@
+// merf_build.cu -- upload-time structure kernels (sm_100a):
+//   K0 occupancy pyramid by max-pooling the finest binary grid,
+//   K1 canonical block allocation of the sparse 3D grid (reading D11),
+//   and the contract_pi helper.
+#include <cstdint>
+#include <cub/device/device_scan.cuh>
+#include <cuda_runtime.h>
+
+#include "merf_device.cuh"
+#include "merf_kernels.h"
+
+namespace merf {
+
+static __host__ __device__ __forceinline__ int ilog2(int v) {
+    int n = 0;
+    while ((1 << n) < v) n++;
+    return n;
+}
+
+// One thread per 32-bit word of the coarse level: OR over the r^3 fine cells of each of its
+// 32 coarse cells.  No atomics; deterministic.
+__global__ void maxpool_bits_kernel(const uint32_t* __restrict__ fine, int f,
+                                    uint32_t* __restrict__ coarse, int N) {
+    int64_t word = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t total = ((int64_t)N * N * N + 31) / 32;
+    if (word >= total) return;
+    const int r = f / N;
+    uint32_t out = 0;
+    for (int b = 0; b < 32; b++) {
+        int64_t lin = word * 32 + b;
+        if (lin >= (int64_t)N * N * N) break;
+        int x = (int)(lin % N), y = (int)((lin / N) % N), z = (int)(lin / ((int64_t)N * N));
+        bool any = false;
+        for (int dz = 0; dz < r && !any; dz++)
+            for (int dy = 0; dy < r && !any; dy++) {
+                // the r fine cells along x of one (z, y) row are contiguous bits
+                int64_t l0 = ((int64_t)(z * r + dz) * f + (y * r + dy)) * f + (int64_t)x * r;
+                for (int dx = 0; dx < r; dx += 32) {
+                    int64_t l = l0 + dx;
+                    int nbits = min(32, r - dx);
+                    int64_t w0 = l >> 5;
+                    int sh = (int)(l & 31);
+                    uint64_t v = __ldg(fine + w0);
+                    if (sh + nbits > 32) v |= (uint64_t)__ldg(fine + w0 + 1) << 32;
+                    uint64_t mask = (nbits == 64) ? ~0ull : ((1ull << nbits) - 1);
+                    if ((v >> sh) & mask) { any = true; break; }
+                }
+            }
+        if (any) out |= 1u << b;
+    }
+    coarse[word] = out;
+}
+
+// Lower trilinear base voxel of lattice coordinate Q on the L grid (clamped, as the render
+// kernel's texel()).
+__device__ __forceinline__ int base_voxel(int64_t Q, int s, int L) {
+    int64_t P = Q + kTwo - (int64_t(1) << (s - 1));
+    int64_t i = P >> s;
+    if (i < 0) i = 0;
+    if (i > L - 2) i = L - 2;
+    return (int)i;
+}
+
+// One thread per finest cell: mark every block slot a sample inside an occupied cell can use.
+__global__ void block_need_kernel(const uint32_t* __restrict__ finest, int N, int L,
+                                  uint8_t* __restrict__ need) {
+    int64_t lin = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (lin >= (int64_t)N * N * N) return;
+    if (!((__ldg(finest + (lin >> 5)) >> (lin & 31)) & 1u)) return;
+    const int cc[3] = {(int)(lin % N), (int)((lin / N) % N), (int)(lin / ((int64_t)N * N))};
+    const int so = kF + 2 - ilog2(N);
+    const int sv = kF + 2 - ilog2(L);
+    const int nb = L / 8;
+    int blo[3], bhi[3];
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+        int lo = (cc[a] == 0) ? 0 : base_voxel(((int64_t)cc[a] << so) - kTwo, sv, L);
+        int hi = (cc[a] == N - 1) ? L - 2 : base_voxel((((int64_t)cc[a] + 1) << so) - kTwo - 1, sv, L);
+        blo[a] = lo >> 3;
+        bhi[a] = hi >> 3;
+    }
+    for (int bz = blo[2]; bz <= bhi[2]; bz++)
+        for (int by = blo[1]; by <= bhi[1]; by++)
+            for (int bx = blo[0]; bx <= bhi[0]; bx++)
+                need[((int64_t)bz * nb + by) * nb + bx] = 1;
+}
+
+__global__ void to_int_kernel(const uint8_t* __restrict__ need, int32_t* __restrict__ flags, int64_t n) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) flags[i] = need[i];
+}
+
+__global__ void number_kernel(const uint8_t* __restrict__ need, const int32_t* __restrict__ scan,
+                              int32_t* __restrict__ index, int64_t n, int64_t* count) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) index[i] = need[i] ? scan[i] : -1;
+    if (i == n - 1) *count = (int64_t)scan[i] + need[i];
+}
+
+__global__ void block_check_kernel(const uint8_t* __restrict__ need, const int32_t* __restrict__ index,
+                                   int64_t n, int64_t n_blocks, unsigned long long* bad) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int32_t v = index[i];
+    bool b = (v < -1) || (v >= n_blocks) || (need[i] && v < 0);
+    if (b) atomicAdd(bad, 1ull);
+}
+
+__global__ void contract_kernel(const double* __restrict__ x, int64_t n, double* __restrict__ y,
+                                int32_t* __restrict__ region) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double p[3] = {x[3 * i], x[3 * i + 1], x[3 * i + 2]}, c[3];
+    int g = region_of(p[0], p[1], p[2]);
+    contract_region(g, p, c);
+    y[3 * i] = c[0];
+    y[3 * i + 1] = c[1];
+    y[3 * i + 2] = c[2];
+    if (region) region[i] = g;
+}
+
+static inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+cudaError_t launch_maxpool_bits(const uint32_t* fine, int f, uint32_t* coarse, int N, cudaStream_t st) {
+    int64_t words = ((int64_t)N * N * N + 31) / 32;
+    maxpool_bits_kernel<<<blocks_for(words, 256), 256, 0, st>>>(fine, f, coarse, N);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_block_need(const uint32_t* finest, int N, int L, uint8_t* need, cudaStream_t st) {
+    int64_t slots = (int64_t)(L / 8) * (L / 8) * (L / 8);
+    cudaError_t e = cudaMemsetAsync(need, 0, slots, st);
+    if (e != cudaSuccess) return e;
+    int64_t cells = (int64_t)N * N * N;
+    block_need_kernel<<<blocks_for(cells, 256), 256, 0, st>>>(finest, N, L, need);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_block_number(const uint8_t* need, int64_t slots, int32_t* index, int64_t* d_count,
+                                void* d_temp, size_t* temp_bytes, int32_t* d_scan, cudaStream_t st) {
+    // d_scan holds 2*slots int32: flags then exclusive scan
+    if (d_temp == nullptr) {
+        return cub::DeviceScan::ExclusiveSum(nullptr, *temp_bytes, (const int32_t*)nullptr,
+                                             (int32_t*)nullptr, (int)slots, st);
+    }
+    to_int_kernel<<<blocks_for(slots, 256), 256, 0, st>>>(need, d_scan, slots);
+    cudaError_t e = cub::DeviceScan::ExclusiveSum(d_temp, *temp_bytes, d_scan, d_scan + slots,
+                                                  (int)slots, st);
+    if (e != cudaSuccess) return e;
+    number_kernel<<<blocks_for(slots, 256), 256, 0, st>>>(need, d_scan + slots, index, slots, d_count);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_block_check(const uint8_t* need, const int32_t* index, int64_t slots,
+                               int64_t n_blocks, unsigned long long* d_bad, cudaStream_t st) {
+    block_check_kernel<<<blocks_for(slots, 256), 256, 0, st>>>(need, index, slots, n_blocks, d_bad);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_contract(const double* x, int64_t n, double* y, int32_t* region, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    contract_kernel<<<blocks_for(n, 256), 256, 0, st>>>(x, n, y, region);
+    return cudaGetLastError();
+}
+
+}  // namespace merf

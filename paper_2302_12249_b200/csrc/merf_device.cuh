@@ -1,0 +1,246 @@
+// merf_device.cuh -- device-side building blocks of libmerf (sm_100a).
+//
+// Canonical fp64 ray setup (reading D8 in DESIGN.md): every fp64 operation that decides
+// the integer lattice (ray generation, region segmentation, contraction of segment
+// endpoints, segment length/direction, llrint to the 2^-40 lattice) uses the _rn
+// intrinsics so that nvcc can never contract a multiply-add into an FMA.  The same
+// IEEE-754 operations in the same order give bit-identical lattices on any conforming
+// implementation (e.g. an fp64 CPU reference), which makes per-ray visited-cell traces
+// comparable bit for bit.  Shading after the lattice is fp32.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/merf.h"
+
+namespace merf {
+
+constexpr int kF = MERF_FIXED_BITS;                       // lattice fraction bits
+constexpr int64_t kOne = int64_t(1) << kF;                // contracted 1.0
+constexpr int64_t kTwo = int64_t(1) << (kF + 1);          // contracted 2.0
+constexpr int kMaxCams = 16;                              // cameras per launch (kernel params)
+constexpr int kMlpFloats = 883;
+
+struct DevScene {
+    const uint8_t* planes;        // [3][R][R][8]
+    const int32_t* block_index;   // [(L/8)^3]
+    const uint8_t* atlas;         // [n_blocks][9][9][9][8]
+    const uint32_t* occ[MERF_MAX_LEVELS];
+    const float* mlp;             // [883]
+    int L, R, nb, n_levels;
+    int level_res[MERF_MAX_LEVELS];
+    int level_shift[MERF_MAX_LEVELS];   // F + 2 - log2(N)
+    int sV, sP;                   // F + 2 - log2(L), F + 2 - log2(R)
+    float kd, ka;                 // 2m/255 (density / appearance)
+    float md, ma;                 // m (density / appearance)
+    int n_src;                    // active sources (V counted only when L > 0)
+    int use_v, use_p[3];
+    double step;                  // Delta (power of two)
+    double lattice_step;          // Delta * 2^F (exact)
+    float step_f, t_min, alpha_skip;
+};
+
+struct CamBatch {
+    merf_camera cam[kMaxCams];
+    int n;
+};
+
+// ------------------------------------------------------------------------------------
+// exact fp64 helpers (never fused)
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double div_rn(double a, double b) { return __ddiv_rn(a, b); }
+
+// region_of: 0 = core iff ||x||_inf <= 1 (D2); else 1 + 2j + (x_j < 0) with j
+// the first index of max |x_j| (D1).
+__device__ __forceinline__ int region_of(double x0, double x1, double x2) {
+    double ax = fabs(x0), ay = fabs(x1), az = fabs(x2);
+    double m = ax;
+    if (ay > m) m = ay;
+    if (az > m) m = az;
+    if (m <= 1.0) return 0;
+    int j = (ax == m) ? 0 : ((ay == m) ? 1 : 2);
+    double xj = (j == 0) ? x0 : ((j == 1) ? x1 : x2);
+    return 1 + 2 * j + (xj < 0.0 ? 1 : 0);
+}
+
+// contract_pi with region g's formula: c_j = s(2 - 1/|x_j|), c_k = x_k/|x_j|.
+__device__ __forceinline__ void contract_region(int g, const double x[3], double c[3]) {
+    if (g == 0) { c[0] = x[0]; c[1] = x[1]; c[2] = x[2]; return; }
+    int j = (g - 1) >> 1;
+    bool neg = ((g - 1) & 1) != 0;
+    double a = fabs(x[j]);
+#pragma unroll
+    for (int k = 0; k < 3; k++) {
+        if (k == j) {
+            double v = sub_rn(2.0, div_rn(1.0, a));
+            c[k] = neg ? -v : v;
+        } else {
+            c[k] = div_rn(x[k], a);
+        }
+    }
+}
+
+// lim_{t->inf} contract_g(o + t d): c_j = 2s, c_k = d_k / |d_j|.
+__device__ __forceinline__ void vanishing_point(int g, const double d[3], double c[3]) {
+    int j = (g - 1) >> 1;
+    bool neg = ((g - 1) & 1) != 0;
+    double a = fabs(d[j]);
+#pragma unroll
+    for (int k = 0; k < 3; k++) c[k] = (k == j) ? (neg ? -2.0 : 2.0) : div_rn(d[k], a);
+}
+
+__device__ __forceinline__ void point_at(const double o[3], const double d[3], double t,
+                                         double x[3]) {
+#pragma unroll
+    for (int k = 0; k < 3; k++) x[k] = add_rn(o[k], mul_rn(t, d[k]));
+}
+
+// Pinhole ray through the centre of pixel (i, j) (reading D18).
+__device__ __forceinline__ void raygen(const merf_camera& c, int i, int j, double o[3],
+                                       double d[3]) {
+    double x0 = div_rn(sub_rn(add_rn((double)i, 0.5), c.cx), c.fx);
+    double x1 = div_rn(sub_rn(add_rn((double)j, 0.5), c.cy), c.fy);
+    double v[3];
+#pragma unroll
+    for (int r = 0; r < 3; r++) {
+        double s = add_rn(mul_rn(c.c2w[4 * r + 0], x0), mul_rn(c.c2w[4 * r + 1], x1));
+        v[r] = add_rn(s, c.c2w[4 * r + 2]);
+    }
+    double n2 = add_rn(add_rn(mul_rn(v[0], v[0]), mul_rn(v[1], v[1])), mul_rn(v[2], v[2]));
+    double n = __dsqrt_rn(n2);
+#pragma unroll
+    for (int r = 0; r < 3; r++) { d[r] = div_rn(v[r], n); o[r] = c.c2w[4 * r + 3]; }
+}
+
+// Region-boundary candidates t > t_near (faces |x_j| = 1, diagonals x_i = +-x_j), sorted
+// ascending with +inf padding.  Sorting network on registers (exact min/max).
+__device__ __forceinline__ void boundary_candidates(const double o[3], const double d[3],
+                                                    double t_near, double cand[12]) {
+    const double inf = __longlong_as_double(0x7ff0000000000000ll);
+#pragma unroll
+    for (int j = 0; j < 3; j++) {
+        double t1 = inf, t2 = inf;
+        if (d[j] != 0.0) {
+            t1 = div_rn(sub_rn(1.0, o[j]), d[j]);
+            t2 = div_rn(sub_rn(-1.0, o[j]), d[j]);
+        }
+        cand[2 * j] = t1;
+        cand[2 * j + 1] = t2;
+    }
+    const int pi_[3] = {0, 0, 1}, pj_[3] = {1, 2, 2};
+#pragma unroll
+    for (int p = 0; p < 3; p++) {
+        int i = pi_[p], j = pj_[p];
+        double den = sub_rn(d[i], d[j]);
+        double t1 = inf, t2 = inf;
+        if (den != 0.0) t1 = div_rn(sub_rn(o[j], o[i]), den);
+        double den2 = add_rn(d[i], d[j]);
+        if (den2 != 0.0) t2 = div_rn(-add_rn(o[i], o[j]), den2);
+        cand[6 + 2 * p] = t1;
+        cand[7 + 2 * p] = t2;
+    }
+#pragma unroll
+    for (int k = 0; k < 12; k++)
+        if (!(cand[k] > t_near) || !isfinite(cand[k])) cand[k] = inf;
+    // odd-even transposition sort (12 elements, fully unrolled -> registers)
+#pragma unroll
+    for (int r = 0; r < 12; r++) {
+#pragma unroll
+        for (int k = (r & 1); k + 1 < 12; k += 2) {
+            double a = cand[k], b = cand[k + 1];
+            cand[k] = fmin(a, b);
+            cand[k + 1] = fmax(a, b);
+        }
+    }
+}
+
+// One contracted segment: lattice origin Qa, step U, sample count K (readings D5-D8).
+struct Segment {
+    int64_t Qa[3];
+    int64_t U[3];
+    int K;
+    int region;
+};
+
+// Returns false if the segment has zero contracted length (dropped).
+__device__ __forceinline__ bool make_segment(const DevScene& S, int g, const double o[3],
+                                             const double d[3], double ta, double tb,
+                                             Segment& seg) {
+    double xa[3], ca[3], cb[3];
+    point_at(o, d, ta, xa);
+    contract_region(g, xa, ca);
+    if (isinf(tb)) {
+        vanishing_point(g, d, cb);
+    } else {
+        double xb[3];
+        point_at(o, d, tb, xb);
+        contract_region(g, xb, cb);
+    }
+    double dx[3];
+#pragma unroll
+    for (int q = 0; q < 3; q++) dx[q] = sub_rn(cb[q], ca[q]);
+    double l2 = add_rn(add_rn(mul_rn(dx[0], dx[0]), mul_rn(dx[1], dx[1])), mul_rn(dx[2], dx[2]));
+    double len = __dsqrt_rn(l2);
+    if (!(len > 0.0)) return false;
+#pragma unroll
+    for (int q = 0; q < 3; q++) {
+        double u = div_rn(dx[q], len);
+        seg.Qa[q] = __double2ll_rn(mul_rn(ca[q], (double)kOne));
+        seg.U[q] = __double2ll_rn(mul_rn(u, S.lattice_step));
+    }
+    seg.K = (int)ceil(div_rn(len, S.step));
+    seg.region = g;
+    return true;
+}
+
+// ------------------------------------------------------------------------------------
+// integer lattice helpers
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ int occ_cell(int64_t Q, int shift, int N) {
+    int64_t c = (Q + kTwo) >> shift;
+    int ci = (int)(c < 0 ? 0 : (c > N - 1 ? N - 1 : c));
+    return ci;
+}
+
+__device__ __forceinline__ bool occ_bit(const uint32_t* bits, int cx, int cy, int cz, int N) {
+    uint32_t lin = ((uint32_t)cz * N + cy) * N + cx;
+    uint32_t w = __ldg(bits + (lin >> 5));
+    return (w >> (lin & 31)) & 1u;
+}
+
+// first k' with Qa + k' U >= face_hi (U > 0)  /  Qa + k' U < face_lo (U < 0); exact.
+__device__ __forceinline__ int64_t exit_axis(int64_t Qa, int64_t U, int64_t face_lo,
+                                             int64_t face_hi) {
+    if (U > 0) {
+        int64_t num = face_hi - Qa;                       // want min e with e*U >= num
+        int64_t e = (int64_t)ceil((double)num / (double)U);
+        while (e * U < num) e++;
+        while ((e - 1) * U >= num) e--;
+        return e;
+    } else {
+        int64_t num = Qa - face_lo;                       // want min e with e*|U| > num
+        int64_t a = -U;
+        int64_t e = (int64_t)floor((double)num / (double)a) + 1;
+        while ((e - 1) * a > num) e--;
+        while (e * a <= num) e++;
+        return e;
+    }
+}
+
+// texel coordinate on a grid of resolution 2^m: lower index and fraction (clamp to edge)
+__device__ __forceinline__ void texel(int64_t Q, int s, int M, int& i0, float& f) {
+    int64_t P = Q + kTwo - (int64_t(1) << (s - 1));
+    int64_t i = P >> s;
+    int64_t rem = P - (i << s);
+    float fr = (s > 24) ? (float)(int)(rem >> (s - 24)) * (1.0f / 16777216.0f)
+                        : (float)(int)rem * __int_as_float((127 - s) << 23);
+    if (i < 0) { i = 0; fr = 0.f; }
+    if (i > M - 2) { i = M - 2; fr = 1.f; }
+    i0 = (int)i;
+    f = fr;
+}
+
+}  // namespace merf

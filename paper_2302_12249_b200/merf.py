@@ -1,0 +1,289 @@
+"""Thin ctypes binding of libmerf.so (include/merf.h).  Argument marshalling only: every
+step of the render path runs in the library's CUDA kernels.  There is no CPU fallback --
+if the library is missing or no CUDA device is present, calls raise.
+
+Function names mirror the C ABI (merf_scene_upload, merf_render, ...).  Device buffers are
+torch CUDA tensors (PyTorch is used for device memory and streams only).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmerf.so")
+
+MERF_OK, MERF_EINVAL, MERF_ENOMEM, MERF_ECUDA, MERF_ENCCL, MERF_EMISMATCH = range(6)
+MERF_RGB_F32, MERF_RGBA_U8 = 0, 1
+MERF_NO_EARLY_TERM, MERF_COUNTERS, MERF_DENSE = 1, 2, 4
+MAX_LEVELS = 4
+
+_STATUS = {1: "MERF_EINVAL", 2: "MERF_ENOMEM", 3: "MERF_ECUDA", 4: "MERF_ENCCL", 5: "MERF_EMISMATCH"}
+
+
+class MerfError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class merf_scene_desc(C.Structure):
+    _fields_ = [("L", C.c_int32), ("R", C.c_int32), ("C", C.c_int32), ("n_levels", C.c_int32),
+                ("level_res", C.c_int32 * MAX_LEVELS),
+                ("m_density", C.c_float), ("m_appearance", C.c_float),
+                ("step", C.c_double), ("t_min", C.c_float), ("alpha_skip", C.c_float),
+                ("source_mask", C.c_uint32)]
+
+
+class merf_camera(C.Structure):
+    _fields_ = [("c2w", C.c_double * 12), ("fx", C.c_double), ("fy", C.c_double),
+                ("cx", C.c_double), ("cy", C.c_double), ("t_near", C.c_double)]
+
+
+class merf_stats(C.Structure):
+    _fields_ = [("rays", C.c_int64), ("segments", C.c_int64), ("evaluated", C.c_int64),
+                ("density_only", C.c_int64), ("skips", C.c_int64), ("missing_blocks", C.c_int64),
+                ("region_segments", C.c_int64 * 7)]
+
+    def as_dict(self):
+        d = {k: int(getattr(self, k)) for k, _ in self._fields_ if k != "region_segments"}
+        d["region_segments"] = [int(v) for v in self.region_segments]
+        return d
+
+
+class merf_scene_info(C.Structure):
+    _fields_ = [("L", C.c_int32), ("R", C.c_int32), ("C", C.c_int32), ("n_levels", C.c_int32),
+                ("level_res", C.c_int32 * MAX_LEVELS), ("n_blocks", C.c_int64),
+                ("canonical_blocks", C.c_int64), ("device_bytes", C.c_int64), ("device", C.c_int32)]
+
+
+_lib = None
+_lock = threading.Lock()
+
+# (name, restype, argtypes) of every exported symbol of include/merf.h
+_vp, _i32, _i64, _u32 = C.c_void_p, C.c_int32, C.c_int64, C.c_uint32
+SIGNATURES = [
+    ("merf_last_error", C.c_char_p, []),
+    ("merf_version", _i32, []),
+    ("merf_scene_upload", C.c_int, [C.POINTER(merf_scene_desc), _vp, _vp, _vp, _i64, _vp, _vp, _i32,
+                                    C.POINTER(_vp)]),
+    ("merf_scene_free", C.c_int, [_vp]),
+    ("merf_scene_info_get", C.c_int, [_vp, C.POINTER(merf_scene_info)]),
+    ("merf_scene_occupancy", C.c_int, [_vp, _i32, _vp, _vp]),
+    ("merf_scene_block_index", C.c_int, [_vp, _vp, _vp]),
+    ("merf_render", C.c_int, [_vp, C.POINTER(merf_camera), _i32, _i32, _i32, _i32, _vp, _u32, _vp,
+                              C.POINTER(merf_stats)]),
+    ("merf_render_host", C.c_int, [_vp, C.POINTER(merf_camera), _i32, _i32, _i32, _i32, _vp, _u32, _vp]),
+    ("merf_render_rays", C.c_int, [_vp, _vp, _vp, _vp, _i64, _vp, _u32, _vp, C.POINTER(merf_stats)]),
+    ("merf_trace", C.c_int, [_vp, C.POINTER(merf_camera), _i32, _vp, _i64, _i32, _vp, _vp, _vp, _u32,
+                             _vp]),
+    ("merf_segments", C.c_int, [_vp, C.POINTER(merf_camera), _i32, _vp, _i64, _i32, _vp, _vp, _vp]),
+    ("merf_contract", C.c_int, [_vp, _i64, _vp, _vp, _vp]),
+    ("merf_build_occupancy", C.c_int, [_vp, C.POINTER(merf_scene_desc), _vp, _vp]),
+    ("merf_build_block_index", C.c_int, [_vp, C.POINTER(merf_scene_desc), _vp, C.POINTER(_i64), _vp]),
+]
+
+
+def lib():
+    """Load libmerf.so (fails loudly if it was not built)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; "
+                                  f"g.build()'` (there is no fallback path)")
+            L = C.CDLL(LIB_PATH)
+            for name, res, args in SIGNATURES:
+                f = getattr(L, name)
+                f.restype = res
+                f.argtypes = args
+            _lib = L
+    return _lib
+
+
+def _check(status):
+    if status != MERF_OK:
+        raise MerfError(status, lib().merf_last_error().decode())
+
+
+def merf_last_error() -> str:
+    return lib().merf_last_error().decode()
+
+
+def merf_version() -> int:
+    return int(lib().merf_version())
+
+
+def _ptr(t):
+    """data pointer of a torch tensor or numpy array (or None)."""
+    if t is None:
+        return None
+    if isinstance(t, np.ndarray):
+        return t.ctypes.data
+    return t.data_ptr()
+
+
+def _stream(stream):
+    import torch
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def make_desc(scene) -> merf_scene_desc:
+    d = merf_scene_desc()
+    d.L, d.R, d.C = int(scene.L), int(scene.R), int(getattr(scene, "C", 8))
+    lv = list(scene.level_res)
+    d.n_levels = len(lv)                 # validated by the library (1..MAX_LEVELS)
+    for i, v in enumerate(lv[:MAX_LEVELS]):
+        d.level_res[i] = int(v)
+    d.m_density = float(getattr(scene, "m_density", 14.0))
+    d.m_appearance = float(getattr(scene, "m_appearance", 7.0))
+    d.step = float(scene.step)
+    d.t_min = float(getattr(scene, "t_min", 2e-4))
+    d.alpha_skip = float(getattr(scene, "alpha_skip", 0.0))
+    d.source_mask = int(getattr(scene, "source_mask", 15))
+    return d
+
+
+def cameras_to_c(cams) -> "C.Array":
+    cams = np.ascontiguousarray(np.asarray(cams, np.float64).reshape(-1, 17))
+    arr = (merf_camera * len(cams))()
+    C.memmove(arr, cams.ctypes.data, cams.nbytes)
+    return arr
+
+
+def merf_scene_upload(scene, device: int = 0, canonical: bool = False) -> int:
+    """Upload host arrays of `scene` (attributes: L, R, level_res, step, planes, block_index,
+    atlas, occ_finest, mlp, ...).  canonical=True passes block_index=NULL.  Returns the handle."""
+    desc = make_desc(scene)
+    planes = np.ascontiguousarray(scene.planes, np.uint8)
+    atlas = np.ascontiguousarray(scene.atlas, np.uint8)
+    bidx = None if canonical else np.ascontiguousarray(scene.block_index, np.int32)
+    occ = np.ascontiguousarray(scene.occ_finest, np.uint32)
+    mlp = np.ascontiguousarray(scene.mlp, np.float32)
+    n_blocks = int(atlas.shape[0]) if atlas.ndim else 0
+    h = C.c_void_p()
+    _check(lib().merf_scene_upload(C.byref(desc), _ptr(planes) if planes.size else None,
+                                   _ptr(bidx) if bidx is not None and bidx.size else None,
+                                   _ptr(atlas) if atlas.size else None, n_blocks, _ptr(occ),
+                                   _ptr(mlp), int(device), C.byref(h)))
+    return h.value
+
+
+def merf_scene_free(handle) -> None:
+    _check(lib().merf_scene_free(handle))
+
+
+def merf_scene_info_get(handle) -> dict:
+    info = merf_scene_info()
+    _check(lib().merf_scene_info_get(handle, C.byref(info)))
+    return dict(L=info.L, R=info.R, n_levels=info.n_levels, level_res=list(info.level_res)[:info.n_levels],
+                n_blocks=info.n_blocks, canonical_blocks=info.canonical_blocks,
+                device_bytes=info.device_bytes, device=info.device)
+
+
+def merf_scene_occupancy(handle, level: int, out, stream=None) -> None:
+    _check(lib().merf_scene_occupancy(handle, int(level), _ptr(out), _stream(stream)))
+
+
+def merf_scene_block_index(handle, out, stream=None) -> None:
+    _check(lib().merf_scene_block_index(handle, _ptr(out), _stream(stream)))
+
+
+def merf_render(handle, cams, W: int, H: int, out, fmt: int = MERF_RGB_F32, flags: int = 0,
+                stream=None, stats: bool = False):
+    """Render frames into the device tensor `out`; returns a stats dict if stats=True."""
+    carr = cameras_to_c(cams)
+    st = merf_stats() if stats else None
+    _check(lib().merf_render(handle, carr, len(carr), int(W), int(H), int(fmt), _ptr(out), int(flags),
+                             _stream(stream), C.byref(st) if st is not None else None))
+    return st.as_dict() if st is not None else None
+
+
+def merf_render_host(handle, cams, W: int, H: int, out_host, fmt: int = MERF_RGBA_U8,
+                     flags: int = 0, stream=None) -> None:
+    """End-to-end: render into scene-owned device staging and copy to the host tensor/array."""
+    carr = cameras_to_c(cams)
+    _check(lib().merf_render_host(handle, carr, len(carr), int(W), int(H), int(fmt), _ptr(out_host),
+                                  int(flags), _stream(stream)))
+
+
+def merf_render_rays(handle, o, d, rgb, t_near=None, flags: int = 0, stream=None, stats: bool = False):
+    st = merf_stats() if stats else None
+    _check(lib().merf_render_rays(handle, _ptr(o), _ptr(d), _ptr(t_near), int(o.shape[0]), _ptr(rgb),
+                                  int(flags), _stream(stream), C.byref(st) if st is not None else None))
+    return st.as_dict() if st is not None else None
+
+
+def merf_trace(handle, cam, W: int, pixel_ids, max_per_ray: int, cells_out, T_out, counts_out,
+               flags: int = 0, stream=None) -> None:
+    carr = cameras_to_c(cam)
+    _check(lib().merf_trace(handle, carr, int(W), _ptr(pixel_ids), int(pixel_ids.shape[0]),
+                            int(max_per_ray), _ptr(cells_out), _ptr(T_out), _ptr(counts_out),
+                            int(flags), _stream(stream)))
+
+
+SEGMENT_DTYPE = np.dtype([("t_a", "<f8"), ("t_b", "<f8"), ("Qa", "<i8", 3), ("U", "<i8", 3),
+                          ("K", "<i4"), ("region", "<i4")])
+
+
+def merf_segments(handle, cam, W: int, pixel_ids, max_seg: int, segs_out, counts_out, stream=None) -> None:
+    """segs_out: device buffer of n * max_seg * 72 bytes (view as SEGMENT_DTYPE on the host)."""
+    carr = cameras_to_c(cam)
+    _check(lib().merf_segments(handle, carr, int(W), _ptr(pixel_ids), int(pixel_ids.shape[0]),
+                               int(max_seg), _ptr(segs_out), _ptr(counts_out), _stream(stream)))
+
+
+def merf_contract(x, y, region=None, stream=None) -> None:
+    _check(lib().merf_contract(_ptr(x), int(x.shape[0]), _ptr(y), _ptr(region), _stream(stream)))
+
+
+def merf_build_occupancy(finest_bits, scene, levels_out, stream=None) -> None:
+    desc = make_desc(scene)
+    _check(lib().merf_build_occupancy(_ptr(finest_bits), C.byref(desc), _ptr(levels_out), _stream(stream)))
+
+
+def merf_build_block_index(finest_bits, scene, index_out, stream=None) -> int:
+    desc = make_desc(scene)
+    n = C.c_int64()
+    _check(lib().merf_build_block_index(_ptr(finest_bits), C.byref(desc), _ptr(index_out), C.byref(n),
+                                        _stream(stream)))
+    return int(n.value)
+
+
+class Scene:
+    """RAII wrapper of a device scene handle."""
+
+    def __init__(self, scene, device: int = 0, canonical: bool = False):
+        self.handle = merf_scene_upload(scene, device=device, canonical=canonical)
+        self.device = device
+
+    def info(self) -> dict:
+        return merf_scene_info_get(self.handle)
+
+    def render(self, cams, W, H, fmt=MERF_RGB_F32, flags=0, out=None, stream=None, stats=False):
+        import torch
+        n = len(np.asarray(cams).reshape(-1, 17))
+        if out is None:
+            shape = (n, H, W, 3) if fmt == MERF_RGB_F32 else (n, H, W, 4)
+            out = torch.empty(shape, dtype=torch.float32 if fmt == MERF_RGB_F32 else torch.uint8,
+                              device=f"cuda:{self.device}")
+        s = merf_render(self.handle, cams, W, H, out, fmt=fmt, flags=flags, stream=stream, stats=stats)
+        return (out, s) if stats else out
+
+    def close(self):
+        if self.handle:
+            merf_scene_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

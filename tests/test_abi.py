@@ -1,0 +1,123 @@
+"""CPU-side checks of the C ABI: the library builds/loads, exports every symbol include/merf.h
+declares, the ctypes struct layouts match the C compiler's, and argument validation rejects
+bad input before touching a device.  No compute calls (no GPU here)."""
+import os
+import re
+import subprocess
+import tempfile
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "merf.h")
+
+
+@pytest.fixture(scope="module")
+def M():
+    from paper_2302_12249_b200 import build
+    build.build()
+    import paper_2302_12249_b200 as M
+    M.lib()
+    return M
+
+
+def _declared():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(merf_[a-z_]+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol(M):
+    names = _declared()
+    assert "merf_render" in names and "merf_scene_upload" in names and len(names) >= 13
+    out = subprocess.run(["nm", "-D", "--defined-only", M.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\bT (merf_\w+)", out))
+    missing = [n for n in names if n not in exported]
+    assert not missing, missing
+    bound = {n for n, _, _ in M.merf.SIGNATURES}
+    assert set(names) == bound, set(names) ^ bound
+
+
+def test_struct_layouts_match_c(M):
+    prog = r'''
+#include <stdio.h>
+#include <stddef.h>
+#include "merf.h"
+int main(void) {
+  printf("%zu %zu %zu %zu %zu %zu %zu\n", sizeof(merf_scene_desc), sizeof(merf_camera),
+         sizeof(merf_stats), sizeof(merf_scene_info), offsetof(merf_scene_desc, step),
+         offsetof(merf_scene_desc, source_mask), offsetof(merf_scene_info, n_blocks));
+  return 0;
+}'''
+    with tempfile.TemporaryDirectory() as d:
+        c = os.path.join(d, "t.c")
+        open(c, "w").write(prog)
+        exe = os.path.join(d, "t")
+        subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), c, "-o", exe])
+        got = list(map(int, subprocess.check_output([exe]).split()))
+    import ctypes as C
+    mm = M.merf
+    expect = [C.sizeof(mm.merf_scene_desc), C.sizeof(mm.merf_camera), C.sizeof(mm.merf_stats),
+              C.sizeof(mm.merf_scene_info), mm.merf_scene_desc.step.offset,
+              mm.merf_scene_desc.source_mask.offset, mm.merf_scene_info.n_blocks.offset]
+    assert got == expect
+
+
+def test_version_and_error_string(M):
+    assert M.merf_version() == 100
+    assert isinstance(M.merf_last_error(), str)
+
+
+def _bad_scene(**kw):
+    from merf_inputs import constant_scene
+    sc = constant_scene()
+    for k, v in kw.items():
+        setattr(sc, k, v)
+    return sc
+
+
+@pytest.mark.parametrize("kw,frag", [
+    (dict(L=12), "L must be"),
+    (dict(R=48), "R must be"),
+    (dict(level_res=(16, 8)), "does not divide"),
+    (dict(level_res=(3, 16)), "power of two"),
+    (dict(step=0.01), "power of two"),
+    (dict(step=-1.0), "step must be"),
+    (dict(C=7), "C must be 8"),
+    (dict(level_res=(2, 4, 8, 16, 32)), "n_levels"),
+])
+def test_upload_rejects_bad_descriptors_without_device(M, kw, frag):
+    sc = _bad_scene(**kw)
+    with pytest.raises(M.MerfError) as e:
+        M.merf_scene_upload(sc, device=0)
+    assert e.value.status == M.MERF_EINVAL
+    assert frag in str(e.value)
+
+
+def test_null_arguments_rejected(M):
+    import ctypes as C
+    L = M.lib()
+    assert L.merf_render(None, None, 1, 8, 8, 0, None, 0, None, None) == M.MERF_EINVAL
+    assert L.merf_render_rays(None, None, None, None, 1, None, 0, None, None) == M.MERF_EINVAL
+    assert L.merf_trace(None, None, 8, None, 1, 4, None, None, None, 0, None) == M.MERF_EINVAL
+    assert L.merf_contract(None, -1, None, None, None) == M.MERF_EINVAL
+    assert L.merf_scene_info_get(None, None) == M.MERF_EINVAL
+    assert L.merf_scene_free(None) == M.MERF_OK
+    assert "NULL" in M.merf_last_error() or M.merf_last_error() == ""
+
+
+def test_ptxas_has_no_spills(M):
+    log = open(os.path.join(ROOT, "paper_2302_12249_b200", "build", "ptxas.log")).read()
+    spills = re.findall(r"(\d+) bytes spill stores", log)
+    assert spills and all(int(s) == 0 for s in spills)
+
+
+def test_product_package_does_not_touch_oracle():
+    # the product path must never import, call or link the oracle (test infrastructure)
+    pkg = os.path.join(ROOT, "paper_2302_12249_b200")
+    for dp, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                s = open(os.path.join(dp, f)).read()
+                assert "oracle" not in s.lower().replace("no oracle", ""), f

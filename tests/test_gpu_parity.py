@@ -1,0 +1,392 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 CPU oracle on the same
+seeded scenes and cameras.  Bar (BASELINE.json north_star): bit-exact occupancy levels,
+block indirection and per-ray visited-cell traces; colour max |err| <= 2e-3 and
+PSNR >= 50 dB."""
+import math
+
+import numpy as np
+import pytest
+
+from conftest import psnr
+from merf_inputs import (make_scene, constant_scene, random_scene, config_cameras,
+                         look_at_camera, unpack_bits, orbit_cameras)
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+TOL = 2e-3
+MIN_PSNR = 50.0
+
+
+@pytest.fixture(scope="module")
+def M():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2302_12249_b200 import build
+    build.build()
+    import paper_2302_12249_b200 as M
+    return M
+
+
+@pytest.fixture(scope="module")
+def c2():
+    return make_scene("c2")
+
+
+def _gpu_frame(M, sc, cams, W, H, flags=0, fmt=0, stats=True):
+    import torch
+    s = M.Scene(sc)
+    out, st = s.render(cams, W, H, fmt=fmt, flags=flags, stats=True)
+    torch.cuda.synchronize()
+    s.close()
+    return out.cpu().numpy(), st
+
+
+def _gpu_trace(M, sc, cam, W, pixels, max_per_ray=2048, flags=0):
+    import torch
+    s = M.Scene(sc)
+    pid = torch.as_tensor(np.asarray(pixels, np.int64), device="cuda")
+    n = len(pixels)
+    cells = torch.zeros((n, max_per_ray), dtype=torch.int64, device="cuda")
+    T = torch.zeros((n, max_per_ray), dtype=torch.float32, device="cuda")
+    cnt = torch.zeros(n, dtype=torch.int32, device="cuda")
+    M.merf_trace(s.handle, cam, W, pid, max_per_ray, cells, T, cnt, flags=flags)
+    torch.cuda.synchronize()
+    s.close()
+    return cells.cpu().numpy().view(np.uint64), T.cpu().numpy(), cnt.cpu().numpy()
+
+
+def _compare_traces(g, o, T_oracle=None, t_min=2e-4):
+    """bit-exact visited cells; with termination on, a length may differ only when the
+    oracle's transmittance at the cut is within 1e-4 relative of t_min (reading D19)."""
+    gc, gT, gn = g
+    oc, on = o["trace_cells"], o["trace_count"]
+    mism = 0
+    for r in range(len(gn)):
+        n = min(gn[r], on[r], gc.shape[1])
+        assert np.array_equal(gc[r, :n], oc[r, :n]), f"ray {r}: first diff at {np.argmax(gc[r,:n] != oc[r,:n])}"
+        if gn[r] != on[r]:
+            mism += 1
+            k = min(gn[r], on[r]) - 1
+            Tcut = o["trace_T"][r, k]
+            assert abs(Tcut - t_min) <= 1e-4 * t_min * 10, (r, gn[r], on[r], Tcut)
+    return mism
+
+
+# ------------------------------------------------------------------------------------
+# structures (bit-exact)
+# ------------------------------------------------------------------------------------
+def test_occupancy_pyramid_bit_exact(M, c2):
+    import torch
+    s = M.Scene(c2)
+    ref = O.build_pyramid(c2.occ_finest, c2.level_res)
+    for lev, N in enumerate(c2.level_res):
+        out = torch.zeros(O.n_words(N), dtype=torch.int32, device="cuda")
+        M.merf_scene_occupancy(s.handle, lev, out)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy().view(np.uint32), ref[lev]), lev
+    # the standalone helper too
+    fin = torch.as_tensor(c2.occ_finest.view(np.int32), device="cuda")
+    tot = sum(O.n_words(N) for N in c2.level_res[:-1])
+    lv = torch.zeros(tot, dtype=torch.int32, device="cuda")
+    M.merf_build_occupancy(fin, c2, lv)
+    torch.cuda.synchronize()
+    assert np.array_equal(lv.cpu().numpy().view(np.uint32), np.concatenate(ref[:-1]))
+    s.close()
+
+
+@pytest.mark.parametrize("case", ["c1", "c2", "rand"])
+def test_block_index_bit_exact(M, c2, case):
+    import torch
+    sc = {"c1": lambda: make_scene("c1"), "c2": lambda: c2,
+          "rand": lambda: random_scene(seed=9, L=64, R=32, level_res=(8, 32))}[case]()
+    ref, n = O.canonical_block_index(sc.occ_finest, sc.level_res[-1], sc.L)
+    fin = torch.as_tensor(sc.occ_finest.view(np.int32), device="cuda")
+    idx = torch.zeros(len(ref), dtype=torch.int32, device="cuda")
+    got_n = M.merf_build_block_index(fin, sc, idx)
+    torch.cuda.synchronize()
+    assert got_n == n
+    assert np.array_equal(idx.cpu().numpy(), ref)
+    s = M.Scene(sc)
+    assert s.info()["canonical_blocks"] == n
+    s.close()
+
+
+def test_upload_rejects_unsound_block_index(M):
+    sc = random_scene(seed=4, L=32, R=32, level_res=(8, 16))
+    ref, n = O.canonical_block_index(sc.occ_finest, 16, 32)
+    bad = sc.block_index.copy()
+    victim = np.nonzero(ref >= 0)[0][0]
+    bad[victim] = -1
+    sc.block_index = bad
+    with pytest.raises(M.MerfError) as e:
+        M.merf_scene_upload(sc)
+    assert e.value.status == M.MERF_EMISMATCH
+    bad = sc.block_index.copy()
+    bad[np.nonzero(bad >= 0)[0][0]] = sc.atlas.shape[0] + 5
+    sc.block_index = bad
+    with pytest.raises(M.MerfError):
+        M.merf_scene_upload(sc)
+
+
+def test_canonical_upload_matches_explicit(M):
+    # atlas supplied in canonical order with block_index = NULL renders identically
+    import torch
+    sc = random_scene(seed=6, L=32, R=32, level_res=(8, 16))
+    ref, n = O.canonical_block_index(sc.occ_finest, 16, 32)
+    # re-pack the atlas in canonical order
+    slots = np.nonzero(ref >= 0)[0]
+    atlas = sc.atlas[sc.block_index[slots]]
+    import copy
+    sc2 = copy.copy(sc)
+    sc2.atlas = np.ascontiguousarray(atlas)
+    sc2.block_index = ref
+    cams, W, H = config_cameras("c1")
+    a, _ = _gpu_frame(M, sc, cams, W, H)
+    s = M.Scene(sc2, canonical=True)
+    b = s.render(cams, W, H)
+    torch.cuda.synchronize()
+    assert np.array_equal(a, b.cpu().numpy())
+    s.close()
+
+
+def test_contract_helper_bit_exact(M):
+    import torch
+    rng = np.random.default_rng(0)
+    x = rng.standard_cauchy((100000, 3)) * rng.uniform(0.1, 10, (100000, 1))
+    x[:10] = [[4, 0, 0], [2, 4, 0], [-3, 1, 0.5], [2, 2, 0], [1, -1, 1], [0, 0, 0], [0, 5, 0],
+              [0, 0, -10], [1e30, 1, 1], [-1e-30, 0, 0]]
+    y_ref, r_ref = O.contract(x)
+    xd = torch.as_tensor(x, device="cuda")
+    yd = torch.empty_like(xd)
+    rd = torch.empty(len(x), dtype=torch.int32, device="cuda")
+    M.merf_contract(xd, yd, rd)
+    torch.cuda.synchronize()
+    assert np.array_equal(yd.cpu().numpy(), y_ref)
+    assert np.array_equal(rd.cpu().numpy(), r_ref)
+
+
+# ------------------------------------------------------------------------------------
+# full frames, C1 (tiny): colour + traces + stats
+# ------------------------------------------------------------------------------------
+def test_c1_frame_colour(M, c1_scene):
+    cams, W, H = config_cameras("c1")
+    got, st = _gpu_frame(M, c1_scene, cams, W, H)
+    ref = O.render(O.OracleScene(c1_scene), cams[0], W, H)
+    g = got[0].reshape(-1, 3)
+    assert np.abs(g - ref["rgb"]).max() <= TOL
+    assert psnr(g, ref["rgb"]) >= MIN_PSNR
+    assert st["rays"] == W * H
+    assert st["evaluated"] == ref["stats"]["evaluated"]
+    assert st["skips"] == ref["stats"]["skips"]
+    assert st["segments"] == ref["stats"]["segments"]
+    assert st["missing_blocks"] == 0
+
+
+@pytest.mark.parametrize("flags", [0, 1])
+def test_c1_traces_bit_exact(M, c1_scene, flags):
+    cams, W, H = config_cameras("c1")
+    pix = np.arange(W * H)
+    g = _gpu_trace(M, c1_scene, cams[0], W, pix, max_per_ray=1024, flags=flags)
+    o = O.render(O.OracleScene(c1_scene), cams[0], W, H, max_trace=1024, flags=flags)
+    mism = _compare_traces(g, o)
+    if flags == 1:
+        assert mism == 0 and np.array_equal(g[2], o["trace_count"])
+    # transmittance after each sample agrees in fp32
+    n = np.minimum(g[2], o["trace_count"])
+    for r in range(0, W * H, 7):
+        assert np.allclose(g[1][r, :n[r]], o["trace_T"][r, :n[r]], atol=2e-5, rtol=1e-4)
+
+
+def test_dense_equals_hierarchical_on_gpu(M, c1_scene):
+    cams, W, H = config_cameras("c1")
+    a, sa = _gpu_frame(M, c1_scene, cams, W, H)
+    b, sb = _gpu_frame(M, c1_scene, cams, W, H, flags=M.MERF_DENSE)
+    assert np.array_equal(a, b)
+    assert sa["evaluated"] == sb["evaluated"] and sb["skips"] == 0
+    pix = np.arange(W * H)
+    ga = _gpu_trace(M, c1_scene, cams[0], W, pix, 1024)
+    gb = _gpu_trace(M, c1_scene, cams[0], W, pix, 1024, flags=M.MERF_DENSE)
+    assert np.array_equal(ga[0], gb[0]) and np.array_equal(ga[2], gb[2])
+
+
+def test_determinism_and_u8(M, c1_scene):
+    cams, W, H = config_cameras("c1")
+    a, _ = _gpu_frame(M, c1_scene, cams, W, H)
+    b, _ = _gpu_frame(M, c1_scene, cams, W, H)
+    assert np.array_equal(a, b)
+    u8, _ = _gpu_frame(M, c1_scene, cams, W, H, fmt=M.MERF_RGBA_U8)
+    assert np.array_equal(u8[..., :3], np.rint(a * 255).astype(np.uint8))
+    assert (u8[..., 3] == 255).all()
+
+
+# ------------------------------------------------------------------------------------
+# random scenes with ragged frame sizes and every source variant
+# ------------------------------------------------------------------------------------
+@pytest.mark.parametrize("seed,mask,WH", [(1, 15, (37, 23)), (2, 15, (64, 48)), (3, 1, (33, 17)),
+                                          (4, 14, (40, 40)), (5, 15, (1, 1)), (6, 5, (23, 61))])
+def test_random_scenes(M, seed, mask, WH):
+    W, H = WH
+    sc = random_scene(seed=seed, L=32, R=64, level_res=(4, 16, 32), occ_fraction=0.2,
+                      source_mask=mask, density_offset=-10)
+    rng = np.random.default_rng(seed)
+    cams = np.stack([look_at_camera(rng.uniform(-1.5, 1.5, 3), target=rng.uniform(-0.5, 0.5, 3),
+                                    W=W, H=H, fov_x_deg=70) for _ in range(3)])
+    got, st = _gpu_frame(M, sc, cams, W, H)
+    osc = O.OracleScene(sc)
+    ev = 0
+    for c in range(3):
+        ref = O.render(osc, cams[c], W, H)
+        g = got[c].reshape(-1, 3)
+        assert np.abs(g - ref["rgb"]).max() <= TOL, c
+        ev += ref["stats"]["evaluated"]
+        o = O.render(osc, cams[c], W, H, max_trace=2048, flags=O.NO_EARLY_TERM)
+        gt = _gpu_trace(M, sc, cams[c], W, np.arange(W * H), 2048, flags=M.MERF_NO_EARLY_TERM)
+        assert np.array_equal(gt[2], o["trace_count"])
+        assert np.array_equal(gt[0], o["trace_cells"])
+    assert st["evaluated"] == ev
+
+
+def test_empty_occupancy(M):
+    N = 16
+    sc = constant_scene(L=16, R=32, level_res=(8, 16), occ=np.zeros((N, N, N), bool))
+    sc.mlp = make_scene("c1").mlp
+    cams, W, H = config_cameras("c1")
+    got, st = _gpu_frame(M, sc, cams, W, H)
+    ref = O.render(O.OracleScene(sc), cams[0], W, H)
+    assert st["evaluated"] == 0
+    assert np.abs(got[0].reshape(-1, 3) - ref["rgb"]).max() <= 1e-5
+
+
+@pytest.mark.parametrize("i", range(5))
+def test_constant_scene_closed_form_on_gpu(M, i):
+    import json, os, torch
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "closed_form.json")))
+    case = g["cases"][i]
+    sc = constant_scene(L=16, R=32, level_res=(8, 16), step=g["delta"], b_d=case["b_d"], b_a=case["b_a"])
+    s = M.Scene(sc)
+    o = torch.zeros((1, 3), dtype=torch.float64, device="cuda")
+    d = torch.tensor([[1.0, 0.0, 0.0]], dtype=torch.float64, device="cuda")
+    rgb = torch.zeros((1, 3), dtype=torch.float32, device="cuda")
+    st = M.merf_render_rays(s.handle, o, d, rgb, stats=True)
+    torch.cuda.synchronize()
+    assert st["evaluated"] == case["n"]
+    assert np.allclose(rgb.cpu().numpy()[0], case["C_zero_mlp"], atol=1e-5)
+    s.close()
+
+
+def test_render_rays_matches_oracle(M, c1_scene):
+    import torch
+    rng = np.random.default_rng(3)
+    n = 5000
+    o = rng.uniform(-1.2, 1.2, (n, 3))
+    d = rng.normal(size=(n, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    tn = rng.uniform(0, 0.3, n)
+    ref = O.render_rays(O.OracleScene(c1_scene), o, d, tn)
+    s = M.Scene(c1_scene)
+    rgb = torch.zeros((n, 3), dtype=torch.float32, device="cuda")
+    st = M.merf_render_rays(s.handle, torch.as_tensor(o, device="cuda"), torch.as_tensor(d, device="cuda"),
+                            rgb, t_near=torch.as_tensor(tn, device="cuda"), stats=True)
+    torch.cuda.synchronize()
+    assert np.abs(rgb.cpu().numpy() - ref["rgb"]).max() <= TOL
+    assert st["evaluated"] == ref["stats"]["evaluated"]
+    s.close()
+
+
+# ------------------------------------------------------------------------------------
+# paper-scale scenes at full size (sampled pixels the oracle computes one by one)
+# ------------------------------------------------------------------------------------
+def _sampled(M, sc, cam, W, H, n=6000, seed=0, trace=512):
+    import torch
+    s = M.Scene(sc)
+    out = s.render(cam[None], W, H)
+    torch.cuda.synchronize()
+    got = out[0].reshape(-1, 3).cpu().numpy()
+    s.close()
+    rng = np.random.default_rng(seed)
+    pix = np.unique(np.concatenate([rng.integers(0, W * H, n), np.arange(0, W * H, 997)]))
+    osc = O.OracleScene(sc)
+    ref = O.render(osc, cam, W, H, pixels=pix)
+    err = np.abs(got[pix] - ref["rgb"])
+    assert err.max() <= TOL, err.max()
+    assert psnr(got[pix], ref["rgb"]) >= MIN_PSNR
+    tp = pix[:trace]
+    o = O.render(osc, cam, W, H, pixels=tp, max_trace=4096, flags=O.NO_EARLY_TERM)
+    g = _gpu_trace(M, sc, cam, W, tp, 4096, flags=M.MERF_NO_EARLY_TERM)
+    assert np.array_equal(g[2], o["trace_count"])
+    assert np.array_equal(g[0], o["trace_cells"])
+    return got
+
+
+def test_c2_paper_scale_sampled(M, c2):
+    cams, W, H = config_cameras("c2")
+    _sampled(M, c2, cams[0], W, H)
+
+
+@pytest.mark.parametrize("pose", [0, 1])
+def test_c3_unbounded_sampled(M, c2, pose):
+    cams, W, H = config_cameras("c3")
+    _sampled(M, c2, cams[pose], W, H, n=4000, seed=pose)
+
+
+def test_c3_all_regions(M, c2):
+    cams, W, H = config_cameras("c3")
+    _, st = _gpu_frame(M, c2, cams, W, H)
+    assert all(v > 0 for v in st["region_segments"]), st["region_segments"]
+
+
+def test_c4_orbit_views_sampled(M, c2):
+    cams = orbit_cameras(256, indices=[0, 77, 200])
+    for k in range(3):
+        _sampled(M, c2, cams[k], 1920, 1080, n=2000, seed=10 + k, trace=128)
+
+
+def test_render_host_equals_render(M, c1_scene):
+    import torch
+    cams = orbit_cameras(16, W=64, H=48, indices=range(9))
+    s = M.Scene(c1_scene)
+    dev = s.render(cams, 64, 48, fmt=M.MERF_RGBA_U8)
+    torch.cuda.synchronize()
+    host = torch.zeros((9, 48, 64, 4), dtype=torch.uint8).pin_memory()
+    M.merf_render_host(s.handle, cams, 64, 48, host, fmt=M.MERF_RGBA_U8)
+    assert torch.equal(dev.cpu(), host)
+    s.close()
+
+
+def _gpu_segments(M, sc, cam, W, pixels, max_seg=8):
+    import torch
+    s = M.Scene(sc)
+    pid = torch.as_tensor(np.asarray(pixels, np.int64), device="cuda")
+    n = len(pixels)
+    segs = torch.zeros(n * max_seg * M.merf.SEGMENT_DTYPE.itemsize, dtype=torch.uint8, device="cuda")
+    cnt = torch.zeros(n, dtype=torch.int32, device="cuda")
+    M.merf_segments(s.handle, cam, W, pid, max_seg, segs, cnt)
+    torch.cuda.synchronize()
+    s.close()
+    return segs.cpu().numpy().view(M.merf.SEGMENT_DTYPE).reshape(n, max_seg), cnt.cpu().numpy()
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c3a", "c3b", "outside"])
+def test_segments_bit_exact(M, c1_scene, cfg):
+    """contracted segments (region, t interval, lattice Qa/U, K) equal the oracle's bit for bit."""
+    if cfg == "c1":
+        cams, W, H = config_cameras("c1")
+        cam, pix = cams[0], np.arange(W * H)
+    elif cfg.startswith("c3"):
+        cams, W, H = config_cameras("c3")
+        cam = cams[0 if cfg == "c3a" else 1]
+        pix = np.random.default_rng(5).integers(0, W * H, 3000)
+    else:
+        W, H = 64, 64
+        cam = look_at_camera((0.0354, 1.3514, -1.0675), target=(0.3, -0.2, 0.1), W=W, H=H, fov_x_deg=90)
+        pix = np.arange(W * H)
+    segs, cnt = _gpu_segments(M, c1_scene, cam, W, pix)
+    for r, p in enumerate(pix):
+        o, d = O.raygen(cam, p % W, p // W)
+        ref = O.segment_ray(o, d, cam[16], c1_scene.step)
+        assert cnt[r] == len(ref), (p, cnt[r], len(ref))
+        for a, b in zip(ref, segs[r]):
+            assert a["region"] == b["region"] and a["K"] == b["K"], p
+            assert a["t_a"] == b["t_a"] and (a["t_b"] == b["t_b"]), p
+            assert np.array_equal(a["Qa"], b["Qa"]) and np.array_equal(a["U"], b["U"]), p
