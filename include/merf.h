@@ -69,7 +69,7 @@ enum {
 };
 
 #define MERF_MAX_LEVELS 4
-#define MERF_FIXED_BITS 40     /* lattice fraction bits F (reading D8)                       */
+#define MERF_FIXED_BITS 28     /* lattice fraction bits F (reading D8): int32 lattice     */
 
 typedef struct {
     int32_t L;                  /* 3D grid resolution: power of two >= 8, or 0 = no grid      */

@@ -25,7 +25,7 @@
 #include <omp.h>
 #endif
 
-#define ORC_F 40                          /* fixed-point fraction bits of the lattice (D8) */
+#define ORC_F 28                          /* fixed-point fraction bits of the lattice (D8) */
 #define ORC_ONE ((int64_t)1 << ORC_F)     /* contracted 1.0 in lattice units              */
 #define ORC_TWO ((int64_t)1 << (ORC_F + 1)) /* contracted 2.0                              */
 #define ORC_MAXSEG 16

@@ -20,7 +20,7 @@ _LIB_PATH = os.path.join(_HERE, "liboracle.so")
 _lock = threading.Lock()
 _lib = None
 
-F_BITS = 40
+F_BITS = 28
 NO_EARLY_TERM = 1
 
 

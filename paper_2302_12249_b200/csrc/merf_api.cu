@@ -185,6 +185,10 @@ extern "C" merf_status merf_scene_upload(const merf_scene_desc* desc, const uint
         UP_TRY(dalloc(s, &d_pl, pb));
         UPC_TRY(cudaMemcpy(d_pl, planes, pb, cudaMemcpyHostToDevice));
         S.planes = d_pl;
+        uint32_t* d_pd;
+        UP_TRY(dalloc(s, &d_pd, (size_t)3 * desc->R * desc->R * 4));
+        UPC_TRY(launch_pack_density(d_pl, desc->R, d_pd, nullptr, 0, nullptr, cs));
+        S.pdens = d_pd;
     }
     // ---- occupancy pyramid (K0)
     const int nl = desc->n_levels;
@@ -244,6 +248,10 @@ extern "C" merf_status merf_scene_upload(const merf_scene_desc* desc, const uint
         if (ab) UPC_TRY(cudaMemcpy(d_at, atlas, ab, cudaMemcpyHostToDevice));
         S.block_index = d_idx;
         S.atlas = d_at;
+        uint2* d_vd;
+        UP_TRY(dalloc(s, &d_vd, (size_t)n_blocks * 512 * 8));
+        if (n_blocks) UPC_TRY(launch_pack_density(nullptr, 0, nullptr, d_at, n_blocks, d_vd, cs));
+        S.vdens = d_vd;
     }
     UPC_TRY(cudaStreamSynchronize(cs));
     cudaStreamDestroy(cs);

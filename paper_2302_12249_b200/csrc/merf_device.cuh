@@ -15,9 +15,11 @@
 
 namespace merf {
 
-constexpr int kF = MERF_FIXED_BITS;                       // lattice fraction bits
+constexpr int kF = MERF_FIXED_BITS;                       // lattice fraction bits (28)
 constexpr int64_t kOne = int64_t(1) << kF;                // contracted 1.0
 constexpr int64_t kTwo = int64_t(1) << (kF + 1);          // contracted 2.0
+constexpr int kTwoI = 1 << (kF + 1);                      // contracted 2.0 (int32 lattice)
+constexpr int kMaxSeg = 7;                                // convex regions: <= 7 per ray
 constexpr int kMaxCams = 16;                              // cameras per launch (kernel params)
 constexpr int kMlpFloats = 883;
 
@@ -25,6 +27,8 @@ struct DevScene {
     const uint8_t* planes;        // [3][R][R][8]
     const int32_t* block_index;   // [(L/8)^3]
     const uint8_t* atlas;         // [n_blocks][9][9][9][8]
+    const uint32_t* pdens;        // [3][R][R] density quads, byte du + 2 dv
+    const uint2* vdens;           // [n_blocks][8][8][8] density octets, byte dx + 2 dy + 4 dz
     const uint32_t* occ[MERF_MAX_LEVELS];
     const float* mlp;             // [883]
     int L, R, nb, n_levels;
@@ -71,7 +75,7 @@ __device__ __forceinline__ void contract_region(int g, const double x[3], double
     if (g == 0) { c[0] = x[0]; c[1] = x[1]; c[2] = x[2]; return; }
     int j = (g - 1) >> 1;
     bool neg = ((g - 1) & 1) != 0;
-    double a = fabs(x[j]);
+    double a = fabs(j == 0 ? x[0] : (j == 1 ? x[1] : x[2]));   // no dynamic indexing
 #pragma unroll
     for (int k = 0; k < 3; k++) {
         if (k == j) {
@@ -87,7 +91,7 @@ __device__ __forceinline__ void contract_region(int g, const double x[3], double
 __device__ __forceinline__ void vanishing_point(int g, const double d[3], double c[3]) {
     int j = (g - 1) >> 1;
     bool neg = ((g - 1) & 1) != 0;
-    double a = fabs(d[j]);
+    double a = fabs(j == 0 ? d[0] : (j == 1 ? d[1] : d[2]));
 #pragma unroll
     for (int k = 0; k < 3; k++) c[k] = (k == j) ? (neg ? -2.0 : 2.0) : div_rn(d[k], a);
 }
@@ -159,8 +163,8 @@ __device__ __forceinline__ void boundary_candidates(const double o[3], const dou
 
 // One contracted segment: lattice origin Qa, step U, sample count K (readings D5-D8).
 struct Segment {
-    int64_t Qa[3];
-    int64_t U[3];
+    int Qa[3];
+    int U[3];
     int K;
     int region;
 };
@@ -188,8 +192,8 @@ __device__ __forceinline__ bool make_segment(const DevScene& S, int g, const dou
 #pragma unroll
     for (int q = 0; q < 3; q++) {
         double u = div_rn(dx[q], len);
-        seg.Qa[q] = __double2ll_rn(mul_rn(ca[q], (double)kOne));
-        seg.U[q] = __double2ll_rn(mul_rn(u, S.lattice_step));
+        seg.Qa[q] = (int)__double2ll_rn(mul_rn(ca[q], (double)kOne));
+        seg.U[q] = (int)__double2ll_rn(mul_rn(u, S.lattice_step));
     }
     seg.K = (int)ceil(div_rn(len, S.step));
     seg.region = g;
@@ -197,12 +201,12 @@ __device__ __forceinline__ bool make_segment(const DevScene& S, int g, const dou
 }
 
 // ------------------------------------------------------------------------------------
-// integer lattice helpers
+// int32 lattice helpers (F = 28: |Q| <= 2^29 + drift, so every position, cell and texel
+// coordinate fits a 32-bit register)
 // ------------------------------------------------------------------------------------
-__device__ __forceinline__ int occ_cell(int64_t Q, int shift, int N) {
-    int64_t c = (Q + kTwo) >> shift;
-    int ci = (int)(c < 0 ? 0 : (c > N - 1 ? N - 1 : c));
-    return ci;
+__device__ __forceinline__ int occ_cell(int Q, int shift, int N) {
+    int c = (Q + kTwoI) >> shift;
+    return min(max(c, 0), N - 1);
 }
 
 __device__ __forceinline__ bool occ_bit(const uint32_t* bits, int cx, int cy, int cz, int N) {
@@ -211,36 +215,44 @@ __device__ __forceinline__ bool occ_bit(const uint32_t* bits, int cx, int cy, in
     return (w >> (lin & 31)) & 1u;
 }
 
-// first k' with Qa + k' U >= face_hi (U > 0)  /  Qa + k' U < face_lo (U < 0); exact.
-__device__ __forceinline__ int64_t exit_axis(int64_t Qa, int64_t U, int64_t face_lo,
-                                             int64_t face_hi) {
-    if (U > 0) {
-        int64_t num = face_hi - Qa;                       // want min e with e*U >= num
-        int64_t e = (int64_t)ceil((double)num / (double)U);
+// First k' >= 0 with Qa + k' U outside [lo, hi) along one axis, capped at K (exact: a float
+// estimate corrected with int32 products, which cannot overflow once capped at K).
+__device__ __forceinline__ int exit_axis(int Qa, int U, int lo, int hi, int K) {
+    if (U > 0) {                                   // min e with Qa + e U >= hi
+        int num = hi - Qa;
+        float ef = ceilf(__fdiv_rn((float)num, (float)U));
+        if (ef >= (float)K) return K;
+        int e = (int)ef;
         while (e * U < num) e++;
         while ((e - 1) * U >= num) e--;
         return e;
-    } else {
-        int64_t num = Qa - face_lo;                       // want min e with e*|U| > num
-        int64_t a = -U;
-        int64_t e = (int64_t)floor((double)num / (double)a) + 1;
+    } else {                                       // min e with Qa + e U < lo
+        int num = Qa - lo;
+        int a = -U;
+        float ef = floorf(__fdiv_rn((float)num, (float)a)) + 1.f;
+        if (ef >= (float)K) return K;
+        int e = (int)ef;
         while ((e - 1) * a > num) e--;
         while (e * a <= num) e++;
         return e;
     }
 }
 
-// texel coordinate on a grid of resolution 2^m: lower index and fraction (clamp to edge)
-__device__ __forceinline__ void texel(int64_t Q, int s, int M, int& i0, float& f) {
-    int64_t P = Q + kTwo - (int64_t(1) << (s - 1));
-    int64_t i = P >> s;
-    int64_t rem = P - (i << s);
-    float fr = (s > 24) ? (float)(int)(rem >> (s - 24)) * (1.0f / 16777216.0f)
-                        : (float)(int)rem * __int_as_float((127 - s) << 23);
+// texel coordinate on a grid of resolution M = 2^m (s = F + 2 - m): lower index, fraction
+// (cell-centred texels, clamp to edge; reading D9)
+__device__ __forceinline__ void texel(int Q, int s, int M, int& i0, float& f) {
+    int P = Q + kTwoI - (1 << (s - 1));
+    int i = P >> s;
+    float fr = (float)(P & ((1 << s) - 1)) * __int_as_float((127 - s) << 23);
     if (i < 0) { i = 0; fr = 0.f; }
     if (i > M - 2) { i = M - 2; fr = 1.f; }
-    i0 = (int)i;
+    i0 = i;
     f = fr;
+}
+
+// byte k of w as an exact float (PRMT builds 2^23 + b, one FADD removes 2^23): no I2F
+__device__ __forceinline__ float byte_f(uint32_t w, int k) {
+    return __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7440u | (unsigned)k)) - 8388608.f;
 }
 
 }  // namespace merf

@@ -34,6 +34,9 @@ cudaError_t launch_block_number(const uint8_t* need, int64_t slots, int32_t* ind
 // upload check: *d_bad += slots that are needed but not stored, or entries out of range
 cudaError_t launch_block_check(const uint8_t* need, const int32_t* index, int64_t slots,
                                int64_t n_blocks, unsigned long long* d_bad, cudaStream_t st);
+// internal density-first layouts (quads per plane texel, octets per grid base voxel)
+cudaError_t launch_pack_density(const uint8_t* planes, int R, uint32_t* pdens, const uint8_t* atlas,
+                                int64_t n_blocks, uint2* vdens, cudaStream_t st);
 cudaError_t launch_contract(const double* x, int64_t n, double* y, int32_t* region, cudaStream_t st);
 
 }  // namespace merf

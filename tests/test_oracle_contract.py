@@ -141,8 +141,8 @@ def test_segments_vs_bruteforce_random_rays():
             assert _collinearity(s, o, d) < 1e-7 * max(1.0, s["len"])
             # lattice: U is u * Delta * 2^F rounded, K = ceil(len / Delta)
             assert s["K"] == math.ceil(s["len"] / step)
-            assert np.abs(s["U"] - s["u"] * step * 2.0 ** 40).max() <= 0.5
-            assert np.abs(s["Qa"] - s["c_a"] * 2.0 ** 40).max() <= 0.5
+            assert np.abs(s["U"] - s["u"] * step * 2.0 ** O.F_BITS).max() <= 0.5
+            assert np.abs(s["Qa"] - s["c_a"] * 2.0 ** O.F_BITS).max() <= 0.5
             assert abs(np.linalg.norm(s["u"]) - 1) < 1e-14
     assert max_seg >= 3
 

@@ -8,7 +8,7 @@ import numpy as np
 from merf_inputs import constant_scene, random_scene, unpack_bits, make_scene
 from oracle import oracle as O
 
-F = 40
+F = O.F_BITS
 
 
 def _Q(c):
