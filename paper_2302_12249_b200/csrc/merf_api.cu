@@ -12,6 +12,7 @@
 #include "../../include/merf.h"
 #include "merf_device.cuh"
 #include "merf_kernels.h"
+#include "merf_render_kernel.cuh"
 
 using namespace merf;
 
@@ -173,6 +174,13 @@ extern "C" merf_status merf_scene_upload(const merf_scene_desc* desc, const uint
 
     cudaStream_t cs;
     UPC_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    {   // keep render workspaces cached in the stream-ordered pool between calls
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    }
     // ---- MLP weights
     float* d_mlp;
     UP_TRY(dalloc(s, &d_mlp, kMlpFloats * sizeof(float)));
@@ -318,17 +326,71 @@ static void to_stats(const unsigned long long* h, merf_stats* st) {
     for (int g = 0; g < 7; g++) st->region_segments[g] = (int64_t)h[6 + g];
 }
 
+// ------------------------------------------------------------------------------------
+// render pipeline orchestration: per chunk of rays, setup -> persistent march -> shade
+// ------------------------------------------------------------------------------------
+static const int64_t kChunkRays = int64_t(1) << 24;   // workspace ~= 232 B per ray in flight
+static const int kViewsPerChunk = 8;
+
+static size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
+
+static merf_status ws_alloc(int64_t n, cudaStream_t st, Workspace& ws, void** base) {
+    const size_t seg = align256((size_t)n * kMaxSeg * 32);
+    const size_t ns = align256((size_t)n);
+    const size_t acc = align256((size_t)n * 32);
+    CUDA_TRY(cudaMallocAsync(base, seg + ns + acc + 256, st));
+    char* b = (char*)*base;
+    ws.seg = (int4*)b;
+    ws.nseg = (uint8_t*)(b + seg);
+    ws.accum = (float4*)(b + seg + ns);
+    ws.queue = (unsigned int*)(b + seg + ns + acc);
+    return MERF_OK;
+}
+
+static merf_status run_chunk(const merf_scene* s, int kf_setup, int kf_march, int kf_shade,
+                             const RaySource& rs, const Workspace& ws, void* out, uint32_t flags,
+                             const TraceArgs& ta, unsigned long long* d_stats, cudaStream_t st) {
+    CUDA_TRY(launch_setup(kf_setup, s->dev, rs, ws, ta, d_stats, st));
+    if (kf_march >= 0) CUDA_TRY(launch_march(kf_march, s->dev, rs.n, ws, flags, ta, d_stats, st));
+    if (kf_shade >= 0) CUDA_TRY(launch_shade(kf_shade, s->dev, rs, ws, out, st));
+    return MERF_OK;
+}
+
+static int march_flags(uint32_t flags, bool count) {
+    return ((flags & MERF_DENSE) ? KF_DENSE : 0) | (count ? KF_COUNT : 0);
+}
+
 static merf_status render_frames(const merf_scene* s, const merf_camera* cams, int32_t n_cams,
                                  int32_t W, int32_t H, int32_t format, void* out, uint32_t flags,
                                  cudaStream_t st, unsigned long long* d_stats) {
     const size_t px_bytes = format == MERF_RGBA_U8 ? 4 : 12;
-    for (int c0 = 0; c0 < n_cams; c0 += kMaxCams) {
-        CamBatch cb;
-        cb.n = n_cams - c0 < kMaxCams ? n_cams - c0 : kMaxCams;
-        for (int i = 0; i < cb.n; i++) cb.cam[i] = cams[c0 + i];
+    RaySource rs{};
+    rs.W = W;
+    rs.H = H;
+    rs.tiles_x = (W + 7) / 8;
+    rs.tiles_per_view = rs.tiles_x * ((H + 3) / 4);
+    const int64_t rays_per_view = (int64_t)rs.tiles_per_view * 32;
+    int vpc = (int)(kChunkRays / rays_per_view);
+    vpc = vpc < 1 ? 1 : (vpc > kViewsPerChunk ? kViewsPerChunk : vpc);
+    if (vpc > n_cams) vpc = n_cams;
+    Workspace ws;
+    void* base = nullptr;
+    merf_status e = ws_alloc(rays_per_view * vpc, st, ws, &base);
+    if (e) return e;
+    const bool count = d_stats != nullptr;
+    for (int c0 = 0; c0 < n_cams; c0 += vpc) {
+        const int nv = n_cams - c0 < vpc ? n_cams - c0 : vpc;
+        rs.cb.n = nv;
+        for (int i = 0; i < nv; i++) rs.cb.cam[i] = cams[c0 + i];
+        rs.ray0 = 0;
+        rs.n = rays_per_view * nv;
         void* o = (char*)out + (size_t)c0 * W * H * px_bytes;
-        CUDA_TRY(launch_render_frames(s->dev, cb, W, H, format, o, flags, d_stats, st));
+        TraceArgs ta{};
+        e = run_chunk(s, count ? KF_COUNT : 0, march_flags(flags, count),
+                      format == MERF_RGBA_U8 ? KF_U8 : 0, rs, ws, o, flags, ta, d_stats, st);
+        if (e) { cudaFreeAsync(base, st); return e; }
     }
+    CUDA_TRY(cudaFreeAsync(base, st));
     return MERF_OK;
 }
 
@@ -412,7 +474,27 @@ extern "C" merf_status merf_render_rays(const merf_scene* s, const double* o, co
         CUDA_TRY(cudaMallocAsync(&d_stats, 16 * sizeof(unsigned long long), st));
         CUDA_TRY(cudaMemsetAsync(d_stats, 0, 16 * sizeof(unsigned long long), st));
     }
-    CUDA_TRY(launch_render_rays(s->dev, o, d, t_near, n, rgb, flags, d_stats, st));
+    {
+        RaySource rs{};
+        rs.o = o;
+        rs.d = d;
+        rs.t_near = t_near;
+        const int64_t chunk = n < kChunkRays ? n : kChunkRays;
+        Workspace ws;
+        void* base = nullptr;
+        merf_status e = ws_alloc(chunk, st, ws, &base);
+        if (e) return e;
+        const bool count = d_stats != nullptr;
+        for (int64_t c0 = 0; c0 < n; c0 += chunk) {
+            rs.ray0 = c0;
+            rs.n = n - c0 < chunk ? n - c0 : chunk;
+            TraceArgs ta{};
+            e = run_chunk(s, KF_RAYS | (count ? KF_COUNT : 0), march_flags(flags, count), KF_RAYS, rs, ws,
+                          rgb, flags, ta, d_stats, st);
+            if (e) { cudaFreeAsync(base, st); return e; }
+        }
+        CUDA_TRY(cudaFreeAsync(base, st));
+    }
     if (d_stats) {
         unsigned long long h[16];
         CUDA_TRY(cudaMemcpyAsync(h, d_stats, sizeof(h), cudaMemcpyDeviceToHost, st));
@@ -432,8 +514,25 @@ extern "C" merf_status merf_trace(const merf_scene* s, const merf_camera* cam, i
         return fail(MERF_EINVAL, "bad n / W / max_per_ray");
     if (!(cam->fx > 0 && cam->fy > 0 && cam->t_near >= 0)) return fail(MERF_EINVAL, "bad camera");
     if (n == 0) return MERF_OK;
-    CUDA_TRY(launch_trace(s->dev, *cam, W, pixel_ids, n, max_per_ray, cells_out, T_out, counts_out,
-                          flags, (cudaStream_t)stream));
+    {
+        cudaStream_t st = (cudaStream_t)stream;
+        RaySource rs{};
+        rs.cb.cam[0] = *cam;
+        rs.cb.n = 1;
+        rs.W = W;
+        rs.pixel_ids = pixel_ids;
+        rs.ray0 = 0;
+        rs.n = n;
+        Workspace ws;
+        void* base = nullptr;
+        merf_status e = ws_alloc(n, st, ws, &base);
+        if (e) return e;
+        TraceArgs ta{cells_out, T_out, counts_out, max_per_ray, nullptr};
+        e = run_chunk(s, KF_TRACE, KF_TRACE | ((flags & MERF_DENSE) ? KF_DENSE : 0), -1, rs, ws, nullptr,
+                      flags, ta, nullptr, st);
+        cudaFreeAsync(base, st);
+        if (e) return e;
+    }
     return MERF_OK;
 }
 
@@ -444,8 +543,18 @@ extern "C" merf_status merf_segments(const merf_scene* s, const merf_camera* cam
     if (n < 0 || n > ((int64_t)1 << 31) || W <= 0 || max_seg < 0) return fail(MERF_EINVAL, "bad n / W / max_seg");
     if (!(cam->fx > 0 && cam->fy > 0 && cam->t_near >= 0)) return fail(MERF_EINVAL, "bad camera");
     if (n == 0) return MERF_OK;
-    CUDA_TRY(launch_segments(s->dev, *cam, W, pixel_ids, n, max_seg, segs_out, counts_out,
-                             (cudaStream_t)stream));
+    {
+        RaySource rs{};
+        rs.cb.cam[0] = *cam;
+        rs.cb.n = 1;
+        rs.W = W;
+        rs.pixel_ids = pixel_ids;
+        rs.ray0 = 0;
+        rs.n = n;
+        Workspace ws{};
+        TraceArgs ta{nullptr, nullptr, counts_out, max_seg, segs_out};
+        CUDA_TRY(launch_setup(KF_SEGS, s->dev, rs, ws, ta, nullptr, (cudaStream_t)stream));
+    }
     return MERF_OK;
 }
 

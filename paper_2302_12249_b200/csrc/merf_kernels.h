@@ -7,22 +7,16 @@
 
 namespace merf {
 
-cudaError_t launch_render_frames(const DevScene& S, const CamBatch& cb, int W, int H, int format,
-                                 void* out, uint32_t rflags, unsigned long long* stats,
-                                 cudaStream_t st);
-cudaError_t launch_render_frames_f32(const DevScene& S, const CamBatch& cb, int W, int H, void* out,
-                                     uint32_t rflags, unsigned long long* stats, cudaStream_t st);
-cudaError_t launch_render_frames_u8(const DevScene& S, const CamBatch& cb, int W, int H, void* out,
-                                    uint32_t rflags, unsigned long long* stats, cudaStream_t st);
-cudaError_t launch_render_rays(const DevScene& S, const double* o, const double* d,
-                               const double* t_near, int64_t n, float* rgb, uint32_t rflags,
-                               unsigned long long* stats, cudaStream_t st);
-cudaError_t launch_trace(const DevScene& S, const merf_camera& cam, int W, const int64_t* pixel_ids,
-                         int64_t n, int max_per_ray, uint64_t* cells, float* T, int32_t* counts,
-                         uint32_t rflags, cudaStream_t st);
-
-cudaError_t launch_segments(const DevScene& S, const merf_camera& cam, int W, const int64_t* pixel_ids,
-                            int64_t n, int max_seg, merf_segment* segs, int32_t* counts, cudaStream_t st);
+// The render pipeline (merf_render_kernel.cuh).  kf = KF_* flags of the variant.
+struct RaySource;
+struct Workspace;
+struct TraceArgs;
+cudaError_t launch_setup(int kf, const DevScene& S, const RaySource& rs, const Workspace& ws,
+                         const TraceArgs& ta, unsigned long long* stats, cudaStream_t st);
+cudaError_t launch_march(int kf, const DevScene& S, int64_t n, const Workspace& ws, uint32_t rflags,
+                         const TraceArgs& ta, unsigned long long* stats, cudaStream_t st);
+cudaError_t launch_shade(int kf, const DevScene& S, const RaySource& rs, const Workspace& ws, void* out,
+                         cudaStream_t st);
 
 // K0: coarse[N^3 bits] = OR over each (f/N)^3 block of fine[f^3 bits]
 cudaError_t launch_maxpool_bits(const uint32_t* fine, int f, uint32_t* coarse, int N, cudaStream_t st);

@@ -1,0 +1,54 @@
+// merf_march.cu -- instantiations + launcher of the persistent march kernel.
+#include <cstdio>
+#include <cstdlib>
+
+#include "merf_render_kernel.cuh"
+
+namespace merf {
+
+static MarchTune march_tune() {
+    static MarchTune t = [] {
+        MarchTune d{32, 16, 16};   // tile-granular scheduling (B200 sweep, tools/tune_sweep.sh)
+        if (const char* e = getenv("MERF_TUNE")) sscanf(e, "%d,%d,%d", &d.refill_min, &d.shade_min, &d.trav_steps);
+        if (d.refill_min < 1) d.refill_min = 1;
+        if (d.refill_min > 32) d.refill_min = 32;
+        if (d.trav_steps < 1) d.trav_steps = 1;
+        return d;
+    }();
+    return t;
+}
+
+template <int KF>
+static cudaError_t march_v(const DevScene& S, int64_t n, const Workspace& ws, uint32_t rflags,
+                           const TraceArgs& ta, unsigned long long* stats, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    static int blocks = 0;                 // persistent grid: resident CTAs x SMs (per variant)
+    if (blocks == 0) {
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_kernel<KF>, kMarchThreads, 0);
+        blocks = sms * (per_sm > 0 ? per_sm : 1);
+    }
+    int64_t need = (n + kMarchThreads - 1) / kMarchThreads;
+    int grid = (int)(need < blocks ? need : blocks);
+    cudaError_t e = cudaMemsetAsync(ws.queue, 0, sizeof(unsigned int), st);
+    if (e != cudaSuccess) return e;
+    march_kernel<KF><<<grid, kMarchThreads, 0, st>>>(S, n, ws, rflags, ta, stats, march_tune());
+    return cudaGetLastError();
+}
+
+cudaError_t launch_march(int kf, const DevScene& S, int64_t n, const Workspace& ws, uint32_t rflags,
+                         const TraceArgs& ta, unsigned long long* stats, cudaStream_t st) {
+    switch (kf & (KF_TRACE | KF_DENSE | KF_COUNT)) {
+        case 0: return march_v<0>(S, n, ws, rflags, ta, stats, st);
+        case KF_COUNT: return march_v<KF_COUNT>(S, n, ws, rflags, ta, stats, st);
+        case KF_DENSE: return march_v<KF_DENSE>(S, n, ws, rflags, ta, stats, st);
+        case KF_DENSE | KF_COUNT: return march_v<KF_DENSE | KF_COUNT>(S, n, ws, rflags, ta, stats, st);
+        case KF_TRACE: return march_v<KF_TRACE>(S, n, ws, rflags, ta, stats, st);
+        case KF_TRACE | KF_DENSE: return march_v<KF_TRACE | KF_DENSE>(S, n, ws, rflags, ta, stats, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace merf

@@ -1,20 +1,21 @@
-// merf_render_kernel.cuh -- the hot path: one fused kernel per batch of views (sm_100a).
+// merf_render_kernel.cuh -- the hot path as a 3-kernel pipeline per chunk of rays (sm_100a).
 //
-// Per ray (Sec. 6), in two phases inside one kernel:
-//  A. setup (fp64, canonical order, reading D8): raygen -> region segmentation of the world
-//     ray into <= 7 contracted segments -> per segment the int32 lattice origin
-//     Qa, step U and sample count K, written to shared memory.  No fp64 state survives A.
-//  B. march (int32 lattice + fp32 shading): Q_k = Qa + k U; coarse-to-fine occupancy probes;
-//     an empty cell jumps to the first lattice sample outside it (the ray-AABB exit);
-//     an evaluated sample reads the DENSITY first -- one 8-byte octet of the block-sparse
-//     grid (through the indirection table) + one 4-byte quad per plane, i.e. 4 loads for the
-//     8 trilinear + 12 bilinear corners (Eq. 5) -- computes alpha = 1 - exp(-tau Delta) and
-//     reads the appearance texels only if alpha > alpha_skip; composite (Eq. 1-2)
-//     with termination at T < 2e-4.
-//  C. deferred MLP h(C_d, F, d) per pixel (Eq. 3) and the store.
-//
-// Layout: one thread per ray; a warp covers an 8 x 4 pixel tile and a CTA 16 x 8 pixels so
-// the 32 rays of a warp are spatially coherent (shared texels, shared occupancy words).
+// Per ray (Sec. 6):
+//  1. setup_kernel (fp64, canonical order, reading D8; one thread per ray, coherent 8x4
+//     pixel tiles): raygen -> region segmentation of the world ray into <= 7 contracted
+//     segments -> per segment the int32 lattice origin Qa, step U and sample
+//     count K -> workspace (32 B per segment).
+//  2. march_kernel (int32 lattice + fp32 shading; persistent warps with ray refill):
+//     Q_k = Qa + k U; coarse-to-fine occupancy probes; an empty cell jumps to the first
+//     lattice sample outside it (the ray-AABB exit).  An evaluated sample reads the
+//     DENSITY first -- one 8-byte octet of the block-sparse grid (through the indirection
+//     table) + one 4-byte quad per plane, i.e. 4 loads for the 8 trilinear + 12 bilinear
+//     corners (Eq. 5) -- computes alpha = 1 - exp(-tau Delta) and reads the appearance
+//     texels only if alpha > alpha_skip; composite (Eq. 1-2) with termination at
+//     T < 2e-4.  Lanes whose ray ended take the next ray of the warp's tile pool, so
+//     the shading code runs with (nearly) full warps regardless of ray-length variance.
+//  3. shade_kernel (coherent tiles): deferred MLP h(C_d, F, d) per pixel (Eq. 3),
+//     C = clamp(C_d + h), store RGB f32 or RGBA8.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -33,14 +34,46 @@ enum : int {
     KF_SEGS = 32,       // record contracted segments only (no marching)
 };
 
-constexpr int kThreads = 128;
+constexpr int kSetupThreads = 128;
+constexpr int kMarchThreads = 256;
+// march scheduling policy (defaults tuned on B200; MERF_TUNE="refill,shade,steps" overrides)
+struct MarchTune {
+    int refill_min;   // refill idle lanes only when at least this many are idle (1..32)
+    int shade_min;    // end a traversal round once this many lanes hold a sample
+    int trav_steps;   // max traversal steps per round
+};
 
-struct RayArgs {
-    const double* o;
+// ------------------------------------------------------------------------------------
+// ray indexing: camera rays are numbered in 8x4-pixel tile order (32 rays per tile, one
+// tile per warp), tiles row-major per view; explicit/trace rays use their list index.
+// ------------------------------------------------------------------------------------
+struct RaySource {
+    CamBatch cb;
+    int W, H, tiles_x, tiles_per_view;
+    int64_t ray0;                // first ray id of this chunk
+    int64_t n;                   // rays in this chunk
+    const double* o;             // explicit rays (KF_RAYS)
     const double* d;
     const double* t_near;
-    const int64_t* pixel_ids;   // trace mode: pixel list of camera 0
-    int64_t n;
+    const int64_t* pixel_ids;    // trace / segments mode: pixel list of camera 0
+};
+
+__device__ __forceinline__ bool ray_pixel(const RaySource& rs, int64_t ray, int& view, int& px, int& py) {
+    const int64_t tile = ray >> 5;
+    const int lane = (int)(ray & 31);
+    view = (int)(tile / rs.tiles_per_view);
+    const int tt = (int)(tile - (int64_t)view * rs.tiles_per_view);
+    const int ty = tt / rs.tiles_x, tx = tt - ty * rs.tiles_x;
+    px = tx * 8 + (lane & 7);
+    py = ty * 4 + (lane >> 3);
+    return px < rs.W && py < rs.H;
+}
+
+struct Workspace {
+    int4* seg;                   // [n][kMaxSeg][2]: (Qa.xyz, K), (U.xyz, region)
+    uint8_t* nseg;               // [n]
+    float4* accum;               // [n][2]: (C_d.rgb, T), (F0..F3)
+    unsigned int* queue;         // ray counter of the persistent march
 };
 
 struct TraceArgs {
@@ -51,13 +84,122 @@ struct TraceArgs {
     merf_segment* segs;
 };
 
+__device__ __forceinline__ void add_stat(unsigned long long* stats, int idx, int v) {
+    unsigned int s = __reduce_add_sync(0xffffffffu, (unsigned)v);
+    if ((threadIdx.x & 31) == 0 && s) atomicAdd(stats + idx, (unsigned long long)s);
+}
+
+// ====================================================================================
+// 1. setup
+// ====================================================================================
+template <int KF>
+__device__ __forceinline__ void emit_segment(const DevScene& S, int g, const double o[3], const double d[3],
+                                             double t_a, double t_b, int64_t r, int64_t ray,
+                                             const Workspace& ws, const TraceArgs& ta, int& nseg,
+                                             unsigned& reg_mask) {
+    Segment sg;
+    if (!make_segment(S, g, o, d, t_a, t_b, sg)) return;   // zero length: dropped
+    if (KF & KF_SEGS) {
+        if (nseg < ta.max_per_ray) {
+            merf_segment rec;
+            rec.t_a = t_a;
+            rec.t_b = t_b;
+#pragma unroll
+            for (int q = 0; q < 3; q++) { rec.Qa[q] = sg.Qa[q]; rec.U[q] = sg.U[q]; }
+            rec.K = sg.K;
+            rec.region = sg.region;
+            ta.segs[ray * ta.max_per_ray + nseg] = rec;
+        }
+    } else if (nseg < kMaxSeg) {
+        int4* p = ws.seg + (r * kMaxSeg + nseg) * 2;
+        p[0] = make_int4(sg.Qa[0], sg.Qa[1], sg.Qa[2], sg.K);
+        p[1] = make_int4(sg.U[0], sg.U[1], sg.U[2], sg.region);
+    }
+    nseg++;
+    reg_mask |= 1u << g;
+}
+
+template <int KF>
+__global__ void __launch_bounds__(kSetupThreads) setup_kernel(DevScene S, RaySource rs, Workspace ws,
+                                                              TraceArgs ta, unsigned long long* stats) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // index within chunk
+    const int64_t ray = rs.ray0 + r;
+    bool valid = r < rs.n;
+    int nseg = 0;
+    unsigned reg_mask = 0;       // regions are convex, so a ray visits each at most once
+    if (valid) {
+        double o[3], d[3], t_near;
+        if (KF & (KF_TRACE | KF_SEGS)) {
+            const int64_t pid = rs.pixel_ids[ray];
+            raygen(rs.cb.cam[0], (int)(pid % rs.W), (int)(pid / rs.W), o, d);
+            t_near = rs.cb.cam[0].t_near;
+        } else if (KF & KF_RAYS) {
+#pragma unroll
+            for (int q = 0; q < 3; q++) { o[q] = rs.o[3 * ray + q]; d[q] = rs.d[3 * ray + q]; }
+            t_near = rs.t_near ? rs.t_near[ray] : 0.0;
+        } else {
+            int view, px, py;
+            valid = ray_pixel(rs, ray, view, px, py);
+            if (valid) {
+                raygen(rs.cb.cam[view], px, py, o, d);
+                t_near = rs.cb.cam[view].t_near;
+            }
+        }
+        if (valid) {
+            double cand[12];
+            boundary_candidates(o, d, t_near, cand);
+            // Walk the sorted boundaries (a register shift queue: constant indices only) and
+            // merge equal-region intervals into segments.
+            double b = t_near, seg_start = t_near;
+            int g_cur = -1;
+            for (int it = 0; it < 13; it++) {
+                for (int pop = 0; pop < 12 && cand[0] <= b; pop++) {
+#pragma unroll
+                    for (int q = 0; q < 11; q++) cand[q] = cand[q + 1];
+                    cand[11] = __longlong_as_double(0x7ff0000000000000ll);
+                }
+                const double nb = cand[0];
+                const bool last = isinf(nb);
+                const double p = last ? add_rn(mul_rn(b, 2.0), 1.0) : mul_rn(add_rn(b, nb), 0.5);
+                double x[3];
+                point_at(o, d, p, x);
+                const int g = region_of(x[0], x[1], x[2]);
+                if (g_cur < 0) {
+                    g_cur = g;
+                    seg_start = b;
+                } else if (g != g_cur) {
+                    emit_segment<KF>(S, g_cur, o, d, seg_start, b, r, ray, ws, ta, nseg, reg_mask);
+                    g_cur = g;
+                    seg_start = b;
+                }
+                if (last) {
+                    emit_segment<KF>(S, g_cur, o, d, seg_start, nb, r, ray, ws, ta, nseg, reg_mask);
+                    break;
+                }
+                b = nb;
+            }
+        }
+    }
+    if (KF & KF_SEGS) {
+        if (r < rs.n) ta.counts[ray] = nseg;
+    } else if (r < rs.n) {
+        ws.nseg[r] = (uint8_t)min(nseg, kMaxSeg);
+    }
+    if (KF & KF_COUNT) {
+        add_stat(stats, 0, valid ? 1 : 0);
+        add_stat(stats, 1, nseg);
+#pragma unroll
+        for (int g = 0; g < 7; g++) add_stat(stats, 6 + g, (reg_mask >> g) & 1u);
+    }
+}
+
+// ====================================================================================
+// 2. march
+// ====================================================================================
 struct RayState {
     float T;
     float cd[3];
     float F[4];
-    int last_cell;          // finest cell of the last evaluated sample (all levels known set)
-    int n_eval;             // evaluated samples (trace index)
-    int c_eval, c_donly, c_skip, c_miss;
 };
 
 __device__ __forceinline__ float sigmoidf_(float x) { return __fdividef(1.0f, 1.0f + __expf(-x)); }
@@ -74,9 +216,11 @@ __device__ __forceinline__ void acc_appearance(float acc[7], uint2 t, float w) {
 }
 
 // Evaluate the field at lattice point (Qx, Qy, Qz) and composite it (Eq. 1-2, 5-7).
-template <int KF>
-__device__ __forceinline__ void shade_sample(const DevScene& S, int Qx, int Qy, int Qz, RayState& st) {
+// Returns 1 if the sample was density-only (alpha <= alpha_skip), 2 if its V block was
+// missing (unsound scene; counted), else 0.
+__device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, int Qz, RayState& st) {
     const int Q[3] = {Qx, Qy, Qz};
+    int ret = 0;
     // ---- density pass: 1 octet (V) + 3 quads (planes)
     int n_src = S.n_src;
     float s0 = 0.f;
@@ -102,7 +246,7 @@ __device__ __forceinline__ void shade_sample(const DevScene& S, int Qx, int Qy, 
             s0 = fmaf(vf[0] * w11, byte_f(oct.y, 3), s0);
         } else {
             n_src -= 1;                    // a missing block contributes nothing
-            if (KF & KF_COUNT) st.c_miss++;
+            ret = 2;
         }
     }
     int pu[3], pv[3];
@@ -158,30 +302,123 @@ __device__ __forceinline__ void shade_sample(const DevScene& S, int Qx, int Qy, 
         for (int c = 0; c < 3; c++) st.cd[c] = fmaf(w, sigmoidf_(fmaf(acc[c], S.ka, off)), st.cd[c]);
 #pragma unroll
         for (int c = 0; c < 4; c++) st.F[c] = fmaf(w, sigmoidf_(fmaf(acc[3 + c], S.ka, off)), st.F[c]);
-    } else if (KF & KF_COUNT) {
-        st.c_donly++;
+    } else if (ret == 0) {
+        ret = 1;
     }
     st.T *= (1.f - alpha);
+    return ret;
 }
 
-// March one contracted segment.  Returns true when the ray terminated.
+// Persistent march.  Every lane owns one ray at a time; a warp takes tiles of 32 rays from
+// the global queue and hands them to idle lanes, so warps stay full while rays of very
+// different lengths finish.  The loop alternates a divergent traversal step (advance to
+// the next occupied sample, crossing segments, finishing/refilling rays) with a converged
+// shading step.
 template <int KF>
-__device__ __forceinline__ bool march_segment(const DevScene& S, int4 qa, int4 uu, int ordinal,
-                                              RayState& st, uint32_t rflags, const TraceArgs& ta,
-                                              int64_t ray) {
+__global__ void __launch_bounds__(kMarchThreads) march_kernel(DevScene S, int64_t n_rays, Workspace ws,
+                                                              uint32_t rflags, TraceArgs ta,
+                                                              unsigned long long* stats, MarchTune tune) {
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt_mask = (1u << lane) - 1u;
     const int nl = S.n_levels;
     const int Nf = S.level_res[nl - 1];
     const int sf = S.level_shift[nl - 1];
     const uint32_t* occ_f = S.occ[nl - 1];
-    const int K = qa.w;
-    int k = 0;
-    while (k < K) {
-        const int Qx = qa.x + k * uu.x, Qy = qa.y + k * uu.y, Qz = qa.z + k * uu.z;
-        const int fx = occ_cell(Qx, sf, Nf), fy = occ_cell(Qy, sf, Nf), fz = occ_cell(Qz, sf, Nf);
-        const int fcell = (fz * Nf + fy) * Nf + fx;
-        if (KF & KF_DENSE) {
-            if (!occ_bit(occ_f, fx, fy, fz, Nf)) { k++; continue; }
-        } else if (fcell != st.last_cell) {
+    const bool early_term = !(rflags & MERF_NO_EARLY_TERM);
+
+    // per-lane ray state
+    int64_t ray = -1;
+    int j = 0, ns = 0, k = 0, last_cell = -1, n_eval = 0;
+    int4 qa = make_int4(0, 0, 0, 0), uu = make_int4(0, 0, 0, 0);
+    RayState st;
+    st.T = 1.f;
+    st.cd[0] = st.cd[1] = st.cd[2] = 0.f;
+    st.F[0] = st.F[1] = st.F[2] = st.F[3] = 0.f;
+    int c_eval = 0, c_donly = 0, c_skip = 0, c_miss = 0;
+    // warp-uniform tile pool [pool_next, pool_end)
+    int64_t pool_next = 0, pool_end = 0;
+    bool exhausted = false;
+
+    auto finish = [&]() {
+        float4* a = ws.accum + ray * 2;
+        a[0] = make_float4(st.cd[0], st.cd[1], st.cd[2], st.T);
+        a[1] = make_float4(st.F[0], st.F[1], st.F[2], st.F[3]);
+        if (KF & KF_TRACE) ta.counts[ray] = n_eval;
+        ray = -1;
+    };
+
+    while (true) {
+        // ---------------- refill idle lanes from the warp's tile pool ----------------
+        unsigned idle = __ballot_sync(FULL, ray < 0);
+        if (__popc(idle) < tune.refill_min && idle != FULL) idle = 0;
+        while (idle && !exhausted) {
+            if (pool_next >= pool_end) {
+                unsigned base = 0;
+                if (lane == 0) base = atomicAdd(ws.queue, 32u);
+                base = __shfl_sync(FULL, base, 0);
+                if ((int64_t)base >= n_rays) { exhausted = true; break; }
+                pool_next = base;
+                pool_end = min((int64_t)base + 32, n_rays);
+            }
+            const int avail = (int)(pool_end - pool_next);
+            const int rank = __popc(idle & lt_mask);
+            if (ray < 0 && rank < avail) {
+                ray = pool_next + rank;
+                ns = ws.nseg[ray];
+                j = 0;
+                k = 0;
+                n_eval = 0;
+                last_cell = -1;
+                st.T = 1.f;
+                st.cd[0] = st.cd[1] = st.cd[2] = 0.f;
+                st.F[0] = st.F[1] = st.F[2] = st.F[3] = 0.f;
+                if (ns > 0) {
+                    const int4* p = ws.seg + (ray * kMaxSeg) * 2;
+                    qa = p[0];
+                    uu = p[1];
+                } else {
+                    qa.w = 0;
+                }
+            }
+            const int took = min(__popc(idle), avail);
+            pool_next += took;
+            idle = __ballot_sync(FULL, ray < 0);
+        }
+        if (__ballot_sync(FULL, ray >= 0) == 0) break;
+
+        // ---------------- traversal: advance lanes towards their next evaluated sample ----
+        // Warp-synchronous steps; the loop ends as soon as enough lanes hold a sample to shade
+        // (lanes in long empty stretches keep skipping in the next round), so one lane's long
+        // skip chain never idles the rest of the warp.
+        bool found = false;
+        int Qx = 0, Qy = 0, Qz = 0, fcell = 0;
+        for (int it = 0; it < tune.trav_steps; it++) {
+            const bool want = ray >= 0 && !found;
+            const unsigned m_want = __ballot_sync(FULL, want);
+            if (m_want == 0) break;
+            if (it > 0 && __popc(__ballot_sync(FULL, found)) >= tune.shade_min) break;
+            if (!want) continue;
+            if (k >= qa.w) {                                  // segment exhausted
+                j++;
+                if (j >= ns) { finish(); continue; }
+                const int4* p = ws.seg + (ray * kMaxSeg + j) * 2;
+                qa = p[0];
+                uu = p[1];
+                k = 0;
+                continue;
+            }
+            Qx = qa.x + k * uu.x;
+            Qy = qa.y + k * uu.y;
+            Qz = qa.z + k * uu.z;
+            const int fx = occ_cell(Qx, sf, Nf), fy = occ_cell(Qy, sf, Nf), fz = occ_cell(Qz, sf, Nf);
+            fcell = (fz * Nf + fy) * Nf + fx;
+            if (KF & KF_DENSE) {
+                if (occ_bit(occ_f, fx, fy, fz, Nf)) found = true;
+                else k++;
+                continue;
+            }
+            if (fcell == last_cell) { found = true; continue; }  // same finest cell: all levels set
             int e = -1;
 #pragma unroll
             for (int lev = 0; lev < MERF_MAX_LEVELS; lev++) {
@@ -191,6 +428,7 @@ __device__ __forceinline__ bool march_segment(const DevScene& S, int4 qa, int4 u
                     const int cx = occ_cell(Qx, sh, N), cy = occ_cell(Qy, sh, N), cz = occ_cell(Qz, sh, N);
                     if (!occ_bit(S.occ[lev], cx, cy, cz, N)) {
                         // jump to the first lattice sample outside this empty cell (ray-AABB exit)
+                        const int K = qa.w;
                         e = K;
                         if (uu.x != 0) e = min(e, exit_axis(qa.x, uu.x, (cx << sh) - kTwoI, ((cx + 1) << sh) - kTwoI, K));
                         if (uu.y != 0) e = min(e, exit_axis(qa.y, uu.y, (cy << sh) - kTwoI, ((cy + 1) << sh) - kTwoI, K));
@@ -199,34 +437,50 @@ __device__ __forceinline__ bool march_segment(const DevScene& S, int4 qa, int4 u
                 }
             }
             if (e >= 0) {
-                k = min(max(k + 1, e), K);
-                if (KF & KF_COUNT) st.c_skip++;
-                continue;
+                k = min(max(k + 1, e), qa.w);
+                if (KF & KF_COUNT) c_skip++;
+            } else {
+                found = true;
             }
         }
-        st.last_cell = fcell;
-        shade_sample<KF>(S, Qx, Qy, Qz, st);
-        if (KF & KF_COUNT) st.c_eval++;
-        if (KF & KF_TRACE) {
-            if (st.n_eval < ta.max_per_ray) {
-                const int64_t idx = ray * ta.max_per_ray + st.n_eval;
-                ta.cells[idx] = ((uint64_t)ordinal << 61) | ((uint64_t)k << 40) | (uint64_t)fcell;
-                if (ta.T) ta.T[idx] = st.T;
+
+        // ---------------- shading (converged) ----------------
+        if (found) {
+            last_cell = fcell;
+            const int kind = shade_sample(S, Qx, Qy, Qz, st);
+            if (KF & KF_COUNT) {
+                c_eval++;
+                c_donly += kind == 1;
+                c_miss += kind == 2;
             }
+            if (KF & KF_TRACE) {
+                if (n_eval < ta.max_per_ray) {
+                    const int64_t idx = ray * ta.max_per_ray + n_eval;
+                    ta.cells[idx] = ((uint64_t)j << 61) | ((uint64_t)k << 40) | (uint64_t)fcell;
+                    if (ta.T) ta.T[idx] = st.T;
+                }
+            }
+            n_eval++;
+            k++;
+            if (early_term && st.T < S.t_min) finish();
         }
-        st.n_eval++;
-        if (!(rflags & MERF_NO_EARLY_TERM) && st.T < S.t_min) return true;
-        k++;
     }
-    return false;
+    if (KF & KF_COUNT) {
+        add_stat(stats, 2, c_eval);
+        add_stat(stats, 3, c_donly);
+        add_stat(stats, 4, c_skip);
+        add_stat(stats, 5, c_miss);
+    }
 }
 
-// Deferred MLP (Eq. 3; 3 layers x 16 hidden, 4 frequencies).
-__device__ __forceinline__ void deferred_mlp(const float* __restrict__ w, const RayState& st,
+// ====================================================================================
+// 3. deferred MLP + store
+// ====================================================================================
+__device__ __forceinline__ void deferred_mlp(const float* __restrict__ w, const float x7[7],
                                              const float d[3], float out[3]) {
     float x[34];
-    x[0] = st.cd[0]; x[1] = st.cd[1]; x[2] = st.cd[2];
-    x[3] = st.F[0]; x[4] = st.F[1]; x[5] = st.F[2]; x[6] = st.F[3];
+#pragma unroll
+    for (int i = 0; i < 7; i++) x[i] = x7[i];
     x[7] = d[0]; x[8] = d[1]; x[9] = d[2];
     int n = 10;
     // sin/cos(2^k d_j), k = 0..3, by angle doubling from |d_j| <= 1 (no slow-path range
@@ -269,163 +523,48 @@ __device__ __forceinline__ void deferred_mlp(const float* __restrict__ w, const 
         float s = b2[o];
 #pragma unroll
         for (int i = 0; i < 16; i++) s = fmaf(W2[o * 16 + i], h1[i], s);
-        out[o] = __fdividef(1.0f, 1.0f + expf(-s));
+        out[o] = __fdividef(1.0f, 1.0f + __expf(-s));
     }
-}
-
-__device__ __forceinline__ void add_stat(unsigned long long* stats, int idx, int v) {
-    unsigned int s = __reduce_add_sync(0xffffffffu, (unsigned)v);
-    if ((threadIdx.x & 31) == 0 && s) atomicAdd(stats + idx, (unsigned long long)s);
 }
 
 template <int KF>
-__global__ void __launch_bounds__(kThreads, 4) render_kernel(DevScene S, CamBatch cb, int W, int H,
-                                                             void* out, uint32_t rflags, RayArgs ra,
-                                                             TraceArgs ta, unsigned long long* stats) {
+__global__ void __launch_bounds__(kSetupThreads) shade_kernel(DevScene S, RaySource rs, Workspace ws,
+                                                              void* out) {
     __shared__ float s_mlp[kMlpFloats];
-    __shared__ int4 s_qa[kMaxSeg][kThreads];    // Qa.xyz, K
-    __shared__ int4 s_u[kMaxSeg][kThreads];     // U.xyz, region
     for (int i = threadIdx.x; i < kMlpFloats; i += blockDim.x) s_mlp[i] = S.mlp[i];
     __syncthreads();
-    const int tid = threadIdx.x;
-
-    bool valid;
-    int64_t ray;
-    int cam_i = 0, px = 0, py = 0;
-    if (KF & (KF_RAYS | KF_TRACE | KF_SEGS)) {
-        ray = (int64_t)blockIdx.x * blockDim.x + tid;
-        valid = ray < ra.n;
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= rs.n) return;
+    const int64_t ray = rs.ray0 + r;
+    float d[3];
+    int64_t out_idx;
+    if (KF & KF_RAYS) {
+#pragma unroll
+        for (int q = 0; q < 3; q++) d[q] = (float)rs.d[3 * ray + q];
+        out_idx = ray;
     } else {
-        const int warp = tid >> 5, lane = tid & 31;
-        px = blockIdx.x * 16 + (warp & 1) * 8 + (lane & 7);
-        py = blockIdx.y * 8 + (warp >> 1) * 4 + (lane >> 3);
-        cam_i = blockIdx.z;
-        valid = px < W && py < H;
-        ray = ((int64_t)cam_i * H + py) * W + px;
+        int view, px, py;
+        if (!ray_pixel(rs, ray, view, px, py)) return;
+        double od[3], dd[3];
+        raygen(rs.cb.cam[view], px, py, od, dd);
+#pragma unroll
+        for (int q = 0; q < 3; q++) d[q] = (float)dd[q];
+        out_idx = ((int64_t)view * rs.H + py) * rs.W + px;
     }
-
-    // ---------------- phase A: fp64 setup -> segments in shared memory ----------------
-    int nseg = 0;
-    unsigned reg_mask = 0;       // regions are convex, so a ray visits each at most once
-    float df[3] = {0.f, 0.f, 1.f};
-    if (valid) {
-        double o[3], d[3], t_near;
-        if (KF & (KF_TRACE | KF_SEGS)) {
-            const int64_t pid = ra.pixel_ids[ray];
-            px = (int)(pid % W);
-            py = (int)(pid / W);
-            raygen(cb.cam[0], px, py, o, d);
-            t_near = cb.cam[0].t_near;
-        } else if (KF & KF_RAYS) {
-#pragma unroll
-            for (int q = 0; q < 3; q++) { o[q] = ra.o[3 * ray + q]; d[q] = ra.d[3 * ray + q]; }
-            t_near = ra.t_near ? ra.t_near[ray] : 0.0;
-        } else {
-            raygen(cb.cam[cam_i], px, py, o, d);
-            t_near = cb.cam[cam_i].t_near;
-        }
-        df[0] = (float)d[0];
-        df[1] = (float)d[1];
-        df[2] = (float)d[2];
-        double cand[12];
-        boundary_candidates(o, d, t_near, cand);
-        // Walk the sorted boundaries; merge equal-region intervals into segments.  The
-        // candidates are consumed as a register shift queue (constant indices only).
-        auto emit = [&](int g, double t_a, double t_b) {
-            Segment sg;
-            if (!make_segment(S, g, o, d, t_a, t_b, sg)) return;   // zero length: dropped
-            if (KF & KF_SEGS) {
-                if (nseg < ta.max_per_ray) {
-                    merf_segment r;
-                    r.t_a = t_a;
-                    r.t_b = t_b;
-#pragma unroll
-                    for (int q = 0; q < 3; q++) { r.Qa[q] = sg.Qa[q]; r.U[q] = sg.U[q]; }
-                    r.K = sg.K;
-                    r.region = sg.region;
-                    ta.segs[ray * ta.max_per_ray + nseg] = r;
-                }
-            } else if (nseg < kMaxSeg) {
-                s_qa[nseg][tid] = make_int4(sg.Qa[0], sg.Qa[1], sg.Qa[2], sg.K);
-                s_u[nseg][tid] = make_int4(sg.U[0], sg.U[1], sg.U[2], sg.region);
-            }
-            nseg++;
-            reg_mask |= 1u << g;
-        };
-        double b = t_near, seg_start = t_near;
-        int g_cur = -1;
-        for (int it = 0; it < 13; it++) {
-            for (int pop = 0; pop < 12 && cand[0] <= b; pop++) {
-#pragma unroll
-                for (int q = 0; q < 11; q++) cand[q] = cand[q + 1];
-                cand[11] = __longlong_as_double(0x7ff0000000000000ll);
-            }
-            const double nb = cand[0];
-            const bool last = isinf(nb);
-            const double p = last ? add_rn(mul_rn(b, 2.0), 1.0) : mul_rn(add_rn(b, nb), 0.5);
-            double x[3];
-            point_at(o, d, p, x);
-            const int g = region_of(x[0], x[1], x[2]);
-            if (g_cur < 0) {
-                g_cur = g;
-                seg_start = b;
-            } else if (g != g_cur) {
-                emit(g_cur, seg_start, b);
-                g_cur = g;
-                seg_start = b;
-            }
-            if (last) {
-                emit(g_cur, seg_start, nb);
-                break;
-            }
-            b = nb;
-        }
-    }
-
-    // ---------------- phase B: march (int32 lattice, fp32 shading) ----------------
-    RayState st;
-    st.T = 1.f;
-#pragma unroll
-    for (int c = 0; c < 3; c++) st.cd[c] = 0.f;
-#pragma unroll
-    for (int c = 0; c < 4; c++) st.F[c] = 0.f;
-    st.last_cell = -1;
-    st.n_eval = 0;
-    st.c_eval = st.c_donly = st.c_skip = st.c_miss = 0;
-    if (valid && !(KF & KF_SEGS)) {
-        const int ns = min(nseg, kMaxSeg);
-        for (int j = 0; j < ns; j++) {
-            if (march_segment<KF>(S, s_qa[j][tid], s_u[j][tid], j, st, rflags, ta, ray)) break;
-        }
-        // ---------------- phase C: deferred MLP + store ----------------
-        float rgb[3];
-        deferred_mlp(s_mlp, st, df, rgb);
-#pragma unroll
-        for (int c = 0; c < 3; c++) rgb[c] = __saturatef(st.cd[c] + rgb[c]);
-        if (KF & KF_TRACE) {
-            ta.counts[ray] = st.n_eval;
-        } else if (KF & KF_U8) {
-            uchar4 v = make_uchar4((unsigned char)__float2int_rn(rgb[0] * 255.f),
-                                   (unsigned char)__float2int_rn(rgb[1] * 255.f),
-                                   (unsigned char)__float2int_rn(rgb[2] * 255.f), 255);
-            reinterpret_cast<uchar4*>(out)[ray] = v;
-        } else {
-            float* o3 = reinterpret_cast<float*>(out) + 3 * ray;
-            o3[0] = rgb[0];
-            o3[1] = rgb[1];
-            o3[2] = rgb[2];
-        }
-    }
-    if ((KF & KF_SEGS) && valid) ta.counts[ray] = nseg;
-    if (KF & KF_COUNT) {
-        add_stat(stats, 0, valid ? 1 : 0);
-        add_stat(stats, 1, nseg);
-        add_stat(stats, 2, st.c_eval);
-        add_stat(stats, 3, st.c_donly);
-        add_stat(stats, 4, st.c_skip);
-        add_stat(stats, 5, st.c_miss);
-#pragma unroll
-        for (int g = 0; g < 7; g++) add_stat(stats, 6 + g, (reg_mask >> g) & 1u);
+    const float4 a0 = ws.accum[r * 2], a1 = ws.accum[r * 2 + 1];
+    const float x7[7] = {a0.x, a0.y, a0.z, a1.x, a1.y, a1.z, a1.w};
+    float h[3];
+    deferred_mlp(s_mlp, x7, d, h);
+    const float c0 = __saturatef(a0.x + h[0]), c1 = __saturatef(a0.y + h[1]), c2 = __saturatef(a0.z + h[2]);
+    if (KF & KF_U8) {
+        reinterpret_cast<uchar4*>(out)[out_idx] =
+            make_uchar4((unsigned char)__float2int_rn(c0 * 255.f), (unsigned char)__float2int_rn(c1 * 255.f),
+                        (unsigned char)__float2int_rn(c2 * 255.f), 255);
+    } else {
+        float* o3 = reinterpret_cast<float*>(out) + 3 * out_idx;
+        o3[0] = c0;
+        o3[1] = c1;
+        o3[2] = c2;
     }
 }
 
