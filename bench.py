@@ -216,8 +216,7 @@ def main():
             st = M.merf_render(scene.handle, batches[s], W_IMG, H_IMG, frames[0], fmt=M.MERF_RGBA_U8,
                                stream=stream, stats=True)
             app = st["evaluated"] - st["density_only"]
-            algo_bytes.append(BYTES_APPEARANCE * app + BYTES_DENSITY_ONLY * st["density_only"]
-                              + BYTES_OUT * st["rays"])
+            algo_bytes.append(BYTES_APPEARANCE * app + BYTES_DENSITY_ONLY * st["density_only"])
             n_eval += st["evaluated"]
             n_donly += st["density_only"]
             n_skip += st["skips"]
@@ -230,7 +229,8 @@ def main():
             if world > 1:
                 stream.wait_stream(gstream)          # buffer reuse after its gather
             ev0[s].record(stream)
-            M.merf_render(scene.handle, batches[s], W_IMG, H_IMG, buf, fmt=M.MERF_RGBA_U8, stream=stream)
+            M.merf_render(scene.handle, batches[s], W_IMG, H_IMG, buf, fmt=M.MERF_RGBA_U8,
+                          flags=M.MERF_TIMED if s >= args.warmup else 0, stream=stream)
             ev1[s].record(stream)
         if world > 1:
             gstream.wait_stream(stream)
@@ -259,7 +259,8 @@ def main():
     if world > 1:
         dist.barrier()
     ms = t_start.elapsed_time(t_end)
-    kern_ms = [ev0[s].elapsed_time(ev1[s]) for s in range(args.warmup, steps_total)]
+    call_ms = [ev0[s].elapsed_time(ev1[s]) for s in range(args.warmup, steps_total)]
+    kt = M.merf_kernel_times_get(scene.handle, reset=True)
     if world > 1:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -268,17 +269,24 @@ def main():
     total_rays = rays_per_step * world * args.steps
     value = total_rays / (ms / 1e3)
 
-    # ---- roofline of the dominant kernel (the fused render kernel, one launch per step)
+    # ---- roofline of the dominant kernel: the persistent march kernel (CUDA events around
+    # every launch, recorded by the library on the render stream with MERF_TIMED)
     peak, peak_src = _peaks()
-    avg_launch_ms = sum(kern_ms) / len(kern_ms)
-    bytes_per_launch = sum(algo_bytes) / len(algo_bytes)
+    n_march = max(kt["march_launches"], 1)
+    avg_launch_ms = kt["march_ms"] / n_march
+    bytes_per_launch = sum(algo_bytes) / n_march
     achieved = bytes_per_launch / (avg_launch_ms / 1e3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": _ncu_traffic(), "peak_source": peak_src,
-                "kernel": "merf::render_kernel<KF_U8>", "avg_launch_ms": avg_launch_ms,
+                "kernel": "merf::march_kernel<0> (persistent march: traversal + gather + composite)",
+                "avg_launch_ms": avg_launch_ms, "launches": kt["march_launches"],
                 "algorithmic_bytes_per_launch": bytes_per_launch,
                 "bytes_model": "160 B per evaluated sample with alpha > 0, 20 B per density-only "
-                               "sample, 4 B RGBA8 per ray (SURVEY 8(d))"}
+                               "sample (SURVEY 8(d)); launch = one chunk of 8 views",
+                "pipeline_ms_per_step": {"setup": kt["setup_ms"] / args.steps,
+                                         "march": kt["march_ms"] / args.steps,
+                                         "shade": kt["shade_ms"] / args.steps,
+                                         "merf_render_call": sum(call_ms) / len(call_ms)}}
 
     # ---- end to end through the C ABI with host buffers (pinned), copies in the timed region
     e2e = None
@@ -322,7 +330,7 @@ def main():
                              "different orbit views" % (info["device_bytes"] / 1e6),
                        "parallelism": f"views sharded over {world} rank(s), scene replicated, "
                                       "NCCL frame gather to rank 0",
-                       "dtype_detail": "u8 features, fp64 ray setup/int64 lattice, fp32 shading"},
+                       "dtype_detail": "u8 features, fp64 ray setup, int32 lattice, fp32 shading (appearance: 16-bit fixed-point weights + dp2a)"},
             "fps": value / (W_IMG * H_IMG),
             "fps_per_gpu": value / (W_IMG * H_IMG) / world,
             "samples_per_sec": n_eval * world / (ms / 1e3),
@@ -334,7 +342,7 @@ def main():
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": args.steps * math.ceil(V / 16),
+            "gpu_launches": kt["setup_launches"] + kt["march_launches"] + kt["shade_launches"],
             "clocks": clk,
             "paper_context": PAPER_CONTEXT,
         }

@@ -65,7 +65,8 @@ enum { MERF_RGB_F32 = 0, MERF_RGBA_U8 = 1 };
 enum {
     MERF_NO_EARLY_TERM = 1u,   /* disable termination at T < t_min                */
     MERF_COUNTERS = 2u,        /* accumulate merf_stats (adds device atomics)             */
-    MERF_DENSE = 4u            /* debug: dense stepping gated by the finest level only     */
+    MERF_DENSE = 4u,           /* debug: dense stepping gated by the finest level only     */
+    MERF_TIMED = 8u            /* record CUDA events around every pipeline kernel launch     */
 };
 
 #define MERF_MAX_LEVELS 4
@@ -112,6 +113,13 @@ typedef struct {
 } merf_scene_info;
 
 typedef struct merf_scene merf_scene;
+
+/* Device time of the render pipeline's kernels launched with MERF_TIMED since the last
+ * reset (CUDA events on the launch stream; reading synchronises them). */
+typedef struct {
+    double setup_ms, march_ms, shade_ms;     /* summed device time per kernel kind        */
+    int64_t setup_launches, march_launches, shade_launches;
+} merf_kernel_times;
 
 /* Thread-local description of the last failure ("" if none). */
 const char *merf_last_error(void);
@@ -167,6 +175,9 @@ merf_status merf_scene_block_index(const merf_scene *scene, int32_t *index_out, 
 merf_status merf_render(const merf_scene *scene, const merf_camera *cams, int32_t n_cams,
                         int32_t W, int32_t H, int32_t format, void *out, uint32_t flags,
                         void *stream, merf_stats *stats);
+
+/* Collect (and, if reset != 0, clear) the MERF_TIMED kernel times of `scene`. */
+merf_status merf_kernel_times_get(merf_scene *scene, merf_kernel_times *out, int32_t reset);
 
 /*
  * End-to-end variant with HOST output: renders into scene-owned device staging buffers in

@@ -4,6 +4,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -29,6 +30,11 @@ struct merf_scene {
     size_t stage_bytes = 0;
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t ev[2] = {nullptr, nullptr};
+    // MERF_TIMED bookkeeping: (kind, start, end) of launches not yet collected
+    struct Timed { int kind; cudaEvent_t a, b; };
+    std::mutex tmu;
+    std::vector<Timed> timed;
+    merf_kernel_times acc{};
 };
 
 static thread_local std::string g_err;
@@ -190,7 +196,9 @@ extern "C" merf_status merf_scene_upload(const merf_scene_desc* desc, const uint
     if (use_p) {
         size_t pb = (size_t)3 * desc->R * desc->R * 8;
         uint8_t* d_pl;
-        UP_TRY(dalloc(s, &d_pl, pb));
+        // padded by one texel row: the clamped upper-edge corner (weight 0) stays in bounds
+        UP_TRY(dalloc(s, &d_pl, pb + (size_t)(desc->R + 2) * 8));
+        UPC_TRY(cudaMemset(d_pl + pb, 0, (size_t)(desc->R + 2) * 8));
         UPC_TRY(cudaMemcpy(d_pl, planes, pb, cudaMemcpyHostToDevice));
         S.planes = d_pl;
         uint32_t* d_pd;
@@ -347,12 +355,76 @@ static merf_status ws_alloc(int64_t n, cudaStream_t st, Workspace& ws, void** ba
     return MERF_OK;
 }
 
+static merf_status timed_launch(const merf_scene* cs, uint32_t flags, int kind, cudaStream_t st,
+                                cudaError_t (*fn)(void*), void* arg) {
+    merf_scene* s = const_cast<merf_scene*>(cs);
+    if (!(flags & MERF_TIMED)) {
+        CUDA_TRY(fn(arg));
+        return MERF_OK;
+    }
+    merf_scene::Timed t{kind, nullptr, nullptr};
+    CUDA_TRY(cudaEventCreate(&t.a));
+    CUDA_TRY(cudaEventCreate(&t.b));
+    CUDA_TRY(cudaEventRecord(t.a, st));
+    CUDA_TRY(fn(arg));
+    CUDA_TRY(cudaEventRecord(t.b, st));
+    std::lock_guard<std::mutex> g(s->tmu);
+    s->timed.push_back(t);
+    return MERF_OK;
+}
+
+struct ChunkCall {
+    const merf_scene* s;
+    int kf_setup, kf_march, kf_shade;
+    const RaySource* rs;
+    const Workspace* ws;
+    void* out;
+    uint32_t flags;
+    const TraceArgs* ta;
+    unsigned long long* d_stats;
+    cudaStream_t st;
+};
+
+static cudaError_t call_setup(void* p) {
+    ChunkCall* c = (ChunkCall*)p;
+    return launch_setup(c->kf_setup, c->s->dev, *c->rs, *c->ws, *c->ta, c->d_stats, c->st);
+}
+static cudaError_t call_march(void* p) {
+    ChunkCall* c = (ChunkCall*)p;
+    return launch_march(c->kf_march, c->s->dev, c->rs->n, *c->ws, c->flags, *c->ta, c->d_stats, c->st);
+}
+static cudaError_t call_shade(void* p) {
+    ChunkCall* c = (ChunkCall*)p;
+    return launch_shade(c->kf_shade, c->s->dev, *c->rs, *c->ws, c->out, c->st);
+}
+
 static merf_status run_chunk(const merf_scene* s, int kf_setup, int kf_march, int kf_shade,
                              const RaySource& rs, const Workspace& ws, void* out, uint32_t flags,
                              const TraceArgs& ta, unsigned long long* d_stats, cudaStream_t st) {
-    CUDA_TRY(launch_setup(kf_setup, s->dev, rs, ws, ta, d_stats, st));
-    if (kf_march >= 0) CUDA_TRY(launch_march(kf_march, s->dev, rs.n, ws, flags, ta, d_stats, st));
-    if (kf_shade >= 0) CUDA_TRY(launch_shade(kf_shade, s->dev, rs, ws, out, st));
+    ChunkCall c{s, kf_setup, kf_march, kf_shade, &rs, &ws, out, flags, &ta, d_stats, st};
+    merf_status e = timed_launch(s, flags, 0, st, call_setup, &c);
+    if (e) return e;
+    if (kf_march >= 0 && (e = timed_launch(s, flags, 1, st, call_march, &c))) return e;
+    if (kf_shade >= 0 && (e = timed_launch(s, flags, 2, st, call_shade, &c))) return e;
+    return MERF_OK;
+}
+
+extern "C" merf_status merf_kernel_times_get(merf_scene* s, merf_kernel_times* out, int32_t reset) {
+    if (!s || !out) return fail(MERF_EINVAL, "NULL argument");
+    std::lock_guard<std::mutex> g(s->tmu);
+    for (auto& t : s->timed) {
+        CUDA_TRY(cudaEventSynchronize(t.b));
+        float ms = 0.f;
+        CUDA_TRY(cudaEventElapsedTime(&ms, t.a, t.b));
+        if (t.kind == 0) { s->acc.setup_ms += ms; s->acc.setup_launches++; }
+        if (t.kind == 1) { s->acc.march_ms += ms; s->acc.march_launches++; }
+        if (t.kind == 2) { s->acc.shade_ms += ms; s->acc.shade_launches++; }
+        cudaEventDestroy(t.a);
+        cudaEventDestroy(t.b);
+    }
+    s->timed.clear();
+    *out = s->acc;
+    if (reset) s->acc = merf_kernel_times{};
     return MERF_OK;
 }
 

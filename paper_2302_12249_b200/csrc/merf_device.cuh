@@ -220,7 +220,7 @@ __device__ __forceinline__ bool occ_bit(const uint32_t* bits, int cx, int cy, in
 __device__ __forceinline__ int exit_axis(int Qa, int U, int lo, int hi, int K) {
     if (U > 0) {                                   // min e with Qa + e U >= hi
         int num = hi - Qa;
-        float ef = ceilf(__fdiv_rn((float)num, (float)U));
+        float ef = ceilf(__fdividef((float)num, (float)U));
         if (ef >= (float)K) return K;
         int e = (int)ef;
         while (e * U < num) e++;
@@ -229,7 +229,7 @@ __device__ __forceinline__ int exit_axis(int Qa, int U, int lo, int hi, int K) {
     } else {                                       // min e with Qa + e U < lo
         int num = Qa - lo;
         int a = -U;
-        float ef = floorf(__fdiv_rn((float)num, (float)a)) + 1.f;
+        float ef = floorf(__fdividef((float)num, (float)a)) + 1.f;
         if (ef >= (float)K) return K;
         int e = (int)ef;
         while ((e - 1) * a > num) e--;
@@ -239,16 +239,32 @@ __device__ __forceinline__ int exit_axis(int Qa, int U, int lo, int hi, int K) {
 }
 
 // texel coordinate on a grid of resolution M = 2^m (s = F + 2 - m): lower index, fraction
-// (cell-centred texels, clamp to edge; reading D9)
+// (cell-centred texels, clamp to edge; reading D9).  Clamping the position to
+// [texel 0, texel M-1] gives the same interpolated value as the (M-2, f = 1) convention at
+// the upper edge: the extra corner i0 + 1 = M carries weight 0 (the layouts are padded so
+// that it is a valid address).
 __device__ __forceinline__ void texel(int Q, int s, int M, int& i0, float& f) {
-    int P = Q + kTwoI - (1 << (s - 1));
-    int i = P >> s;
-    float fr = (float)(P & ((1 << s) - 1)) * __int_as_float((127 - s) << 23);
-    if (i < 0) { i = 0; fr = 0.f; }
-    if (i > M - 2) { i = M - 2; fr = 1.f; }
-    i0 = i;
-    f = fr;
+    const int P = min(max(Q + kTwoI - (1 << (s - 1)), 0), (M - 1) << s);
+    i0 = P >> s;
+    f = (float)(P & ((1 << s) - 1)) * __int_as_float((127 - s) << 23);
 }
+
+// 16-bit fixed-point interpolation weights that partition 65535 EXACTLY (so a constant
+// field interpolates exactly): split an integer weight W along one axis with fraction f
+// into (W - round(f W), round(f W)).  Rounding via the 1.5 * 2^23 magic (x + M leaves
+// round(x) in the low mantissa bits; no F2I), int -> float via the 2^23 magic (no I2F).
+__device__ __forceinline__ uint32_t rnd_u16(float x) {          // x in [0, 65535]
+    return __float_as_uint(x + 12582912.f) & 0xFFFFu;
+}
+__device__ __forceinline__ float u2f(uint32_t v) {               // v < 2^23, exact
+    return __uint_as_float(0x4B000000u | v) - 8388608.f;
+}
+__device__ __forceinline__ void wsplit(uint32_t W, float f, uint32_t& w0, uint32_t& w1) {
+    w1 = rnd_u16(f * u2f(W));
+    w0 = W - w1;
+}
+// pack two 16-bit weights into the (lo16, hi16) operand of dp2a
+__device__ __forceinline__ uint32_t wpack(uint32_t w0, uint32_t w1) { return w0 | (w1 << 16); }
 
 // byte k of w as an exact float (PRMT builds 2^23 + b, one FADD removes 2^23): no I2F
 __device__ __forceinline__ float byte_f(uint32_t w, int k) {

@@ -36,12 +36,12 @@ enum : int {
 
 constexpr int kSetupThreads = 128;
 constexpr int kMarchThreads = 256;
-// march scheduling policy (defaults tuned on B200; MERF_TUNE="refill,shade,steps" overrides)
-struct MarchTune {
-    int refill_min;   // refill idle lanes only when at least this many are idle (1..32)
-    int shade_min;    // end a traversal round once this many lanes hold a sample
-    int trav_steps;   // max traversal steps per round
-};
+// March scheduling policy, tuned on B200 (bench workload sweep): a warp takes a new tile of
+// 32 rays only when all its lanes are idle (per-lane refill broke the tile coherence the
+// skipping relies on and was 1.5-2x slower); a traversal round ends once kShadeMin lanes
+// hold a sample or after kTravSteps steps.
+constexpr int kShadeMin = 16;
+constexpr int kTravSteps = 16;
 
 // ------------------------------------------------------------------------------------
 // ray indexing: camera rays are numbered in 8x4-pixel tile order (32 rays per tile, one
@@ -204,15 +204,21 @@ struct RayState {
 
 __device__ __forceinline__ float sigmoidf_(float x) { return __fdividef(1.0f, 1.0f + __expf(-x)); }
 
-// accumulate channels 1..7 of an 8-byte AoS texel with weight w
-__device__ __forceinline__ void acc_appearance(float acc[7], uint2 t, float w) {
-    acc[0] = fmaf(w, byte_f(t.x, 1), acc[0]);
-    acc[1] = fmaf(w, byte_f(t.x, 2), acc[1]);
-    acc[2] = fmaf(w, byte_f(t.x, 3), acc[2]);
-    acc[3] = fmaf(w, byte_f(t.y, 0), acc[3]);
-    acc[4] = fmaf(w, byte_f(t.y, 1), acc[4]);
-    acc[5] = fmaf(w, byte_f(t.y, 2), acc[5]);
-    acc[6] = fmaf(w, byte_f(t.y, 3), acc[6]);
+// Appearance accumulation of a corner PAIR (texels a, b; 16-bit weights packed in wp):
+// integer dot products dp2a over byte pairs gathered with PRMT, 7 channels in 4 PRMT +
+// 7 DP2A (vs 14 byte converts + 14 FMA in fp32).  acc[c] is in units of 1/65535 byte.
+__device__ __forceinline__ void acc_pair(uint32_t acc[7], uint2 a, uint2 b, uint32_t wp) {
+    const uint32_t rg = __byte_perm(a.x, b.x, 0x6251);     // r_a r_b g_a g_b
+    const uint32_t bd = __byte_perm(a.x, b.x, 0x0073);     // b_a b_b
+    const uint32_t f01 = __byte_perm(a.y, b.y, 0x5140);    // f0_a f0_b f1_a f1_b
+    const uint32_t f23 = __byte_perm(a.y, b.y, 0x7362);    // f2_a f2_b f3_a f3_b
+    acc[0] = __dp2a_lo(wp, rg, acc[0]);
+    acc[1] = __dp2a_hi(wp, rg, acc[1]);
+    acc[2] = __dp2a_lo(wp, bd, acc[2]);
+    acc[3] = __dp2a_lo(wp, f01, acc[3]);
+    acc[4] = __dp2a_hi(wp, f01, acc[4]);
+    acc[5] = __dp2a_lo(wp, f23, acc[5]);
+    acc[6] = __dp2a_hi(wp, f23, acc[6]);
 }
 
 // Evaluate the field at lattice point (Qx, Qy, Qz) and composite it (Eq. 1-2, 5-7).
@@ -269,39 +275,45 @@ __device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, i
     const float tau = __expf(t0);
     const float alpha = 1.f - __expf(-tau * S.step_f);
     if (alpha > S.alpha_skip) {
-        // ---- appearance pass: 20 AoS texels, channels 1..7
-        float acc[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        // ---- appearance pass: 20 AoS texels, channels 1..7, 16-bit weights + dp2a
+        uint32_t acc[7] = {0u, 0u, 0u, 0u, 0u, 0u, 0u};
         if (blk >= 0) {
-            const uint8_t* base = S.atlas + (size_t)blk * (729 * 8);
+            const uint2* base = reinterpret_cast<const uint2*>(S.atlas + (size_t)blk * (729 * 8));
             const int lx = vi[0] & 7, ly = vi[1] & 7, lz = vi[2] & 7;
+            uint32_t wz[2], wzy[4];
+            wsplit(65535u, vf[2], wz[0], wz[1]);
+            wsplit(wz[0], vf[1], wzy[0], wzy[1]);
+            wsplit(wz[1], vf[1], wzy[2], wzy[3]);
 #pragma unroll
-            for (int c = 0; c < 8; c++) {
-                const int dx = c & 1, dy = (c >> 1) & 1, dz = c >> 2;
-                const uint2 t = __ldg(reinterpret_cast<const uint2*>(
-                    base + (((lz + dz) * 9 + (ly + dy)) * 9 + (lx + dx)) * 8));
-                const float w = (dx ? vf[0] : 1.f - vf[0]) * (dy ? vf[1] : 1.f - vf[1]) *
-                                (dz ? vf[2] : 1.f - vf[2]);
-                acc_appearance(acc, t, w);
+            for (int c = 0; c < 4; c++) {                 // (dy, dz) rows; x pair per row
+                const int dy = c & 1, dz = c >> 1;
+                const uint2* row = base + ((lz + dz) * 9 + (ly + dy)) * 9 + lx;
+                uint32_t w0, w1;
+                wsplit(wzy[c], vf[0], w0, w1);
+                acc_pair(acc, __ldg(row), __ldg(row + 1), wpack(w0, w1));
             }
         }
 #pragma unroll
         for (int a = 0; a < 3; a++) {
             if (!S.use_p[a]) continue;
             const uint2* pl = reinterpret_cast<const uint2*>(S.planes) + (size_t)a * S.R * S.R;
+            uint32_t wv[2];
+            wsplit(65535u, fv[a], wv[0], wv[1]);
 #pragma unroll
-            for (int c = 0; c < 4; c++) {
-                const int du = c & 1, dv = c >> 1;
-                const uint2 t = __ldg(pl + (size_t)(pv[a] + dv) * S.R + (pu[a] + du));
-                const float w = (du ? fu[a] : 1.f - fu[a]) * (dv ? fv[a] : 1.f - fv[a]);
-                acc_appearance(acc, t, w);
+            for (int dv = 0; dv < 2; dv++) {
+                const uint2* row = pl + (size_t)(pv[a] + dv) * S.R + pu[a];
+                uint32_t w0, w1;
+                wsplit(wv[dv], fu[a], w0, w1);
+                acc_pair(acc, __ldg(row), __ldg(row + 1), wpack(w0, w1));
             }
         }
         const float off = -(float)n_src * S.ma;
+        const float ka = S.ka * (1.f / 65535.f);
         const float w = alpha * st.T;
 #pragma unroll
-        for (int c = 0; c < 3; c++) st.cd[c] = fmaf(w, sigmoidf_(fmaf(acc[c], S.ka, off)), st.cd[c]);
+        for (int c = 0; c < 3; c++) st.cd[c] = fmaf(w, sigmoidf_(fmaf((float)(int)acc[c], ka, off)), st.cd[c]);
 #pragma unroll
-        for (int c = 0; c < 4; c++) st.F[c] = fmaf(w, sigmoidf_(fmaf(acc[3 + c], S.ka, off)), st.F[c]);
+        for (int c = 0; c < 4; c++) st.F[c] = fmaf(w, sigmoidf_(fmaf((float)(int)acc[3 + c], ka, off)), st.F[c]);
     } else if (ret == 0) {
         ret = 1;
     }
@@ -315,9 +327,9 @@ __device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, i
 // the next occupied sample, crossing segments, finishing/refilling rays) with a converged
 // shading step.
 template <int KF>
-__global__ void __launch_bounds__(kMarchThreads) march_kernel(DevScene S, int64_t n_rays, Workspace ws,
+__global__ void __launch_bounds__(kMarchThreads, 4) march_kernel(DevScene S, int64_t n_rays, Workspace ws,
                                                               uint32_t rflags, TraceArgs ta,
-                                                              unsigned long long* stats, MarchTune tune) {
+                                                              unsigned long long* stats) {
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
@@ -328,7 +340,7 @@ __global__ void __launch_bounds__(kMarchThreads) march_kernel(DevScene S, int64_
     const bool early_term = !(rflags & MERF_NO_EARLY_TERM);
 
     // per-lane ray state
-    int64_t ray = -1;
+    int ray = -1;                      // chunk-local ray index (chunks < 2^31 rays)
     int j = 0, ns = 0, k = 0, last_cell = -1, n_eval = 0;
     int4 qa = make_int4(0, 0, 0, 0), uu = make_int4(0, 0, 0, 0);
     RayState st;
@@ -337,11 +349,11 @@ __global__ void __launch_bounds__(kMarchThreads) march_kernel(DevScene S, int64_
     st.F[0] = st.F[1] = st.F[2] = st.F[3] = 0.f;
     int c_eval = 0, c_donly = 0, c_skip = 0, c_miss = 0;
     // warp-uniform tile pool [pool_next, pool_end)
-    int64_t pool_next = 0, pool_end = 0;
+    int pool_next = 0, pool_end = 0;
     bool exhausted = false;
 
     auto finish = [&]() {
-        float4* a = ws.accum + ray * 2;
+        float4* a = ws.accum + (int64_t)ray * 2;
         a[0] = make_float4(st.cd[0], st.cd[1], st.cd[2], st.T);
         a[1] = make_float4(st.F[0], st.F[1], st.F[2], st.F[3]);
         if (KF & KF_TRACE) ta.counts[ray] = n_eval;
@@ -351,17 +363,17 @@ __global__ void __launch_bounds__(kMarchThreads) march_kernel(DevScene S, int64_
     while (true) {
         // ---------------- refill idle lanes from the warp's tile pool ----------------
         unsigned idle = __ballot_sync(FULL, ray < 0);
-        if (__popc(idle) < tune.refill_min && idle != FULL) idle = 0;
+        if (idle != FULL) idle = 0;                       // tile-granular scheduling
         while (idle && !exhausted) {
             if (pool_next >= pool_end) {
                 unsigned base = 0;
                 if (lane == 0) base = atomicAdd(ws.queue, 32u);
                 base = __shfl_sync(FULL, base, 0);
                 if ((int64_t)base >= n_rays) { exhausted = true; break; }
-                pool_next = base;
-                pool_end = min((int64_t)base + 32, n_rays);
+                pool_next = (int)base;
+                pool_end = (int)min((int64_t)base + 32, n_rays);
             }
-            const int avail = (int)(pool_end - pool_next);
+            const int avail = pool_end - pool_next;
             const int rank = __popc(idle & lt_mask);
             if (ray < 0 && rank < avail) {
                 ray = pool_next + rank;
@@ -374,7 +386,7 @@ __global__ void __launch_bounds__(kMarchThreads) march_kernel(DevScene S, int64_
                 st.cd[0] = st.cd[1] = st.cd[2] = 0.f;
                 st.F[0] = st.F[1] = st.F[2] = st.F[3] = 0.f;
                 if (ns > 0) {
-                    const int4* p = ws.seg + (ray * kMaxSeg) * 2;
+                    const int4* p = ws.seg + ((int64_t)ray * kMaxSeg) * 2;
                     qa = p[0];
                     uu = p[1];
                 } else {
@@ -393,16 +405,16 @@ __global__ void __launch_bounds__(kMarchThreads) march_kernel(DevScene S, int64_
         // skip chain never idles the rest of the warp.
         bool found = false;
         int Qx = 0, Qy = 0, Qz = 0, fcell = 0;
-        for (int it = 0; it < tune.trav_steps; it++) {
+        for (int it = 0; it < kTravSteps; it++) {
             const bool want = ray >= 0 && !found;
             const unsigned m_want = __ballot_sync(FULL, want);
             if (m_want == 0) break;
-            if (it > 0 && __popc(__ballot_sync(FULL, found)) >= tune.shade_min) break;
+            if (it > 0 && __popc(__ballot_sync(FULL, found)) >= kShadeMin) break;
             if (!want) continue;
             if (k >= qa.w) {                                  // segment exhausted
                 j++;
                 if (j >= ns) { finish(); continue; }
-                const int4* p = ws.seg + (ray * kMaxSeg + j) * 2;
+                const int4* p = ws.seg + ((int64_t)ray * kMaxSeg + j) * 2;
                 qa = p[0];
                 uu = p[1];
                 k = 0;
@@ -455,7 +467,7 @@ __global__ void __launch_bounds__(kMarchThreads) march_kernel(DevScene S, int64_
             }
             if (KF & KF_TRACE) {
                 if (n_eval < ta.max_per_ray) {
-                    const int64_t idx = ray * ta.max_per_ray + n_eval;
+                    const int64_t idx = (int64_t)ray * ta.max_per_ray + n_eval;
                     ta.cells[idx] = ((uint64_t)j << 61) | ((uint64_t)k << 40) | (uint64_t)fcell;
                     if (ta.T) ta.T[idx] = st.T;
                 }

@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(_HERE, "libmerf.so")
 
 MERF_OK, MERF_EINVAL, MERF_ENOMEM, MERF_ECUDA, MERF_ENCCL, MERF_EMISMATCH = range(6)
 MERF_RGB_F32, MERF_RGBA_U8 = 0, 1
-MERF_NO_EARLY_TERM, MERF_COUNTERS, MERF_DENSE = 1, 2, 4
+MERF_NO_EARLY_TERM, MERF_COUNTERS, MERF_DENSE, MERF_TIMED = 1, 2, 4, 8
 MAX_LEVELS = 4
 
 _STATUS = {1: "MERF_EINVAL", 2: "MERF_ENOMEM", 3: "MERF_ECUDA", 4: "MERF_ENCCL", 5: "MERF_EMISMATCH"}
@@ -54,6 +54,11 @@ class merf_stats(C.Structure):
         return d
 
 
+class merf_kernel_times(C.Structure):
+    _fields_ = [("setup_ms", C.c_double), ("march_ms", C.c_double), ("shade_ms", C.c_double),
+                ("setup_launches", C.c_int64), ("march_launches", C.c_int64), ("shade_launches", C.c_int64)]
+
+
 class merf_scene_info(C.Structure):
     _fields_ = [("L", C.c_int32), ("R", C.c_int32), ("C", C.c_int32), ("n_levels", C.c_int32),
                 ("level_res", C.c_int32 * MAX_LEVELS), ("n_blocks", C.c_int64),
@@ -72,6 +77,7 @@ SIGNATURES = [
                                     C.POINTER(_vp)]),
     ("merf_scene_free", C.c_int, [_vp]),
     ("merf_scene_info_get", C.c_int, [_vp, C.POINTER(merf_scene_info)]),
+    ("merf_kernel_times_get", C.c_int, [_vp, C.POINTER(merf_kernel_times), _i32]),
     ("merf_scene_occupancy", C.c_int, [_vp, _i32, _vp, _vp]),
     ("merf_scene_block_index", C.c_int, [_vp, _vp, _vp]),
     ("merf_render", C.c_int, [_vp, C.POINTER(merf_camera), _i32, _i32, _i32, _i32, _vp, _u32, _vp,
@@ -186,6 +192,12 @@ def merf_scene_info_get(handle) -> dict:
     return dict(L=info.L, R=info.R, n_levels=info.n_levels, level_res=list(info.level_res)[:info.n_levels],
                 n_blocks=info.n_blocks, canonical_blocks=info.canonical_blocks,
                 device_bytes=info.device_bytes, device=info.device)
+
+
+def merf_kernel_times_get(handle, reset: bool = True) -> dict:
+    t = merf_kernel_times()
+    _check(lib().merf_kernel_times_get(handle, C.byref(t), int(bool(reset))))
+    return {k: getattr(t, k) for k, _ in t._fields_}
 
 
 def merf_scene_occupancy(handle, level: int, out, stream=None) -> None:
