@@ -278,7 +278,7 @@ def main():
     achieved = bytes_per_launch / (avg_launch_ms / 1e3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": _ncu_traffic(), "peak_source": peak_src,
-                "kernel": "merf::march_kernel<0> (persistent march: traversal + gather + composite)",
+                "kernel": "merf::march_kernel<KF_ALLSRC> (persistent march: traversal + gather + composite)",
                 "avg_launch_ms": avg_launch_ms, "launches": kt["march_launches"],
                 "algorithmic_bytes_per_launch": bytes_per_launch,
                 "bytes_model": "160 B per evaluated sample with alpha > 0, 20 B per density-only "

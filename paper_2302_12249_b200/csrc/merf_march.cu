@@ -28,6 +28,10 @@ static cudaError_t march_v(const DevScene& S, int64_t n, const Workspace& ws, ui
 
 cudaError_t launch_march(int kf, const DevScene& S, int64_t n, const Workspace& ws, uint32_t rflags,
                          const TraceArgs& ta, unsigned long long* stats, cudaStream_t st) {
+    if (S.n_src == 4 && !(kf & (KF_TRACE | KF_DENSE))) {    // production variants
+        if (kf & KF_COUNT) return march_v<KF_ALLSRC | KF_COUNT>(S, n, ws, rflags, ta, stats, st);
+        return march_v<KF_ALLSRC>(S, n, ws, rflags, ta, stats, st);
+    }
     switch (kf & (KF_TRACE | KF_DENSE | KF_COUNT)) {
         case 0: return march_v<0>(S, n, ws, rflags, ta, stats, st);
         case KF_COUNT: return march_v<KF_COUNT>(S, n, ws, rflags, ta, stats, st);

@@ -32,6 +32,7 @@ enum : int {
     KF_U8 = 8,          // RGBA8 output
     KF_DENSE = 16,      // dense stepping gated by the finest level (debug)
     KF_SEGS = 32,       // record contracted segments only (no marching)
+    KF_ALLSRC = 64,     // all four sources present (compile-time; the production variant)
 };
 
 constexpr int kSetupThreads = 128;
@@ -223,21 +224,29 @@ __device__ __forceinline__ void acc_pair(uint32_t acc[7], uint2 a, uint2 b, uint
 
 // Evaluate the field at lattice point (Qx, Qy, Qz) and composite it (Eq. 1-2, 5-7).
 // Returns 1 if the sample was density-only (alpha <= alpha_skip), 2 if its V block was
-// missing (unsound scene; counted), else 0.
-__device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, int Qz, RayState& st) {
+// missing (unsound scene; counted), else 0.  `bslot`/`bblk` cache the last block lookup.
+template <int KF>
+__device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, int Qz, RayState& st,
+                                            int& bslot, int& bblk) {
+    constexpr bool ALL = (KF & KF_ALLSRC) != 0;
+    const bool use_v = ALL || S.use_v;
     const int Q[3] = {Qx, Qy, Qz};
     int ret = 0;
     // ---- density pass: 1 octet (V) + 3 quads (planes)
-    int n_src = S.n_src;
+    int n_src = ALL ? 4 : S.n_src;
     float s0 = 0.f;
     int vi[3] = {0, 0, 0};
     float vf[3] = {0.f, 0.f, 0.f};
     int blk = -1;
-    if (S.use_v) {
+    if (use_v) {
 #pragma unroll
         for (int a = 0; a < 3; a++) texel(Q[a], S.sV, S.L, vi[a], vf[a]);
         const int slot = ((vi[2] >> 3) * S.nb + (vi[1] >> 3)) * S.nb + (vi[0] >> 3);
-        blk = __ldg(S.block_index + slot);
+        if (slot != bslot) {                              // blocks change every ~8 voxels
+            bslot = slot;
+            bblk = __ldg(S.block_index + slot);
+        }
+        blk = bblk;
         if (blk >= 0) {
             const uint2 oct = __ldg(S.vdens + ((size_t)blk * 512 + ((vi[2] & 7) * 8 + (vi[1] & 7)) * 8 + (vi[0] & 7)));
             const float gx = 1.f - vf[0], gy = 1.f - vf[1], gz = 1.f - vf[2];
@@ -255,21 +264,26 @@ __device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, i
             ret = 2;
         }
     }
-    int pu[3], pv[3];
-    float fu[3], fv[3];
+    // plane texel coordinates: each axis feeds two planes (P_x(y,z), P_y(x,z), P_z(x,y))
+    int pi[3] = {0, 0, 0};
+    float pf[3] = {0.f, 0.f, 0.f};
+    const bool any_p = ALL || S.R > 0;
+    if (any_p) {
+#pragma unroll
+        for (int a = 0; a < 3; a++) texel(Q[a], S.sP, S.R, pi[a], pf[a]);
+    }
 #pragma unroll
     for (int a = 0; a < 3; a++) {
-        if (!S.use_p[a]) continue;
+        if (!(ALL || S.use_p[a])) continue;
         const int ua = (a == 0) ? 1 : 0;
         const int va = (a == 2) ? 1 : 2;
-        texel(Q[ua], S.sP, S.R, pu[a], fu[a]);
-        texel(Q[va], S.sP, S.R, pv[a], fv[a]);
-        const uint32_t quad = __ldg(S.pdens + ((size_t)a * S.R + pv[a]) * S.R + pu[a]);
-        const float gu = 1.f - fu[a], gv = 1.f - fv[a];
+        const uint32_t quad = __ldg(S.pdens + ((size_t)a * S.R + pi[va]) * S.R + pi[ua]);
+        const float fu = pf[ua], fv = pf[va];
+        const float gu = 1.f - fu, gv = 1.f - fv;
         s0 = fmaf(gu * gv, byte_f(quad, 0), s0);
-        s0 = fmaf(fu[a] * gv, byte_f(quad, 1), s0);
-        s0 = fmaf(gu * fv[a], byte_f(quad, 2), s0);
-        s0 = fmaf(fu[a] * fv[a], byte_f(quad, 3), s0);
+        s0 = fmaf(fu * gv, byte_f(quad, 1), s0);
+        s0 = fmaf(gu * fv, byte_f(quad, 2), s0);
+        s0 = fmaf(fu * fv, byte_f(quad, 3), s0);
     }
     const float t0 = fmaf(s0, S.kd, -(float)n_src * S.md);
     const float tau = __expf(t0);
@@ -295,15 +309,17 @@ __device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, i
         }
 #pragma unroll
         for (int a = 0; a < 3; a++) {
-            if (!S.use_p[a]) continue;
+            if (!(ALL || S.use_p[a])) continue;
+            const int ua = (a == 0) ? 1 : 0;
+            const int va = (a == 2) ? 1 : 2;
             const uint2* pl = reinterpret_cast<const uint2*>(S.planes) + (size_t)a * S.R * S.R;
             uint32_t wv[2];
-            wsplit(65535u, fv[a], wv[0], wv[1]);
+            wsplit(65535u, pf[va], wv[0], wv[1]);
 #pragma unroll
             for (int dv = 0; dv < 2; dv++) {
-                const uint2* row = pl + (size_t)(pv[a] + dv) * S.R + pu[a];
+                const uint2* row = pl + (size_t)(pi[va] + dv) * S.R + pi[ua];
                 uint32_t w0, w1;
-                wsplit(wv[dv], fu[a], w0, w1);
+                wsplit(wv[dv], pf[ua], w0, w1);
                 acc_pair(acc, __ldg(row), __ldg(row + 1), wpack(w0, w1));
             }
         }
@@ -341,6 +357,7 @@ __global__ void __launch_bounds__(kMarchThreads, 4) march_kernel(DevScene S, int
 
     // per-lane ray state
     int ray = -1;                      // chunk-local ray index (chunks < 2^31 rays)
+    int bslot = -1, bblk = -1;         // last V block lookup
     int j = 0, ns = 0, k = 0, last_cell = -1, n_eval = 0;
     int4 qa = make_int4(0, 0, 0, 0), uu = make_int4(0, 0, 0, 0);
     RayState st;
@@ -459,7 +476,7 @@ __global__ void __launch_bounds__(kMarchThreads, 4) march_kernel(DevScene S, int
         // ---------------- shading (converged) ----------------
         if (found) {
             last_cell = fcell;
-            const int kind = shade_sample(S, Qx, Qy, Qz, st);
+            const int kind = shade_sample<KF>(S, Qx, Qy, Qz, st, bslot, bblk);
             if (KF & KF_COUNT) {
                 c_eval++;
                 c_donly += kind == 1;
