@@ -358,8 +358,8 @@ def make_scene(config: str = "c1", seed: int = SEED, L=None, R=None, level_res=N
                     pass
                 planes[a, :, :, ch] = v.reshape(R, R).astype(np.uint8)
         if L == 0:
-            # planes-only variant: the density ramp must come from the planes (3 sources)
-            planes = _planes_only_density(world, planes, R, w_ramp, density_bias)
+            # planes-only variant: the density must come from the planes (3 sources)
+            planes = _planes_only_density(occ, planes, R)
     else:
         planes = np.zeros((3, 0, 0, Cn), np.uint8)
         R = 0
@@ -369,24 +369,21 @@ def make_scene(config: str = "c1", seed: int = SEED, L=None, R=None, level_res=N
     return sc
 
 
-def _planes_only_density(world, planes, R, w_ramp, density_bias):
-    """Planes-only variant: each plane holds the max over its axis of the V density ramp,
-    a crude projection so that the 3-plane sum still has surfaces."""
-    g = (np.arange(R) + 0.5) * (4.0 / R) - 2.0
+def _planes_only_density(occ, planes, R):
+    """Planes-only variant (config 5, "without 3D grid"): each plane's density is the
+    projection of the finest occupancy along its normal (upsampled to R x R): +2 where some
+    occupied cell projects, -14 elsewhere, so the 3-plane sum (6) is high only where all three
+    projections agree.  A synthetic stand-in for throughput/parity (quality is out of scope)."""
+    N = occ.shape[0]
+    rep = max(R // N, 1)
     for a in range(3):
-        # sample 64 depths along the plane normal and keep the largest target density
-        best = np.full((R, R), -14.0)
-        for dd in np.linspace(-1.9, 1.9, 64):
-            V, U = np.meshgrid(g, g, indexing="ij")
-            pts = np.zeros((R * R, 3))
-            ua, va = [(1, 2), (0, 2), (0, 1)][a]
-            pts[:, ua] = U.ravel()
-            pts[:, va] = V.ravel()
-            pts[:, a] = dd
-            d, _ = contracted_distance(world, pts)
-            t0 = np.clip(-d / w_ramp, -1.0, 1.0) * 14.0 / 3.0 + density_bias / 3.0
-            best = np.maximum(best, t0.reshape(R, R))
-        planes[a, :, :, 0] = _encode(best, 14.0)
+        proj = occ.any(axis=2 - a)            # occ is [z, y, x]; axis a -> numpy axis 2 - a
+        # P_x is indexed [z][y], P_y [z][x], P_z [y][x]: proj rows are the higher axis
+        img = np.repeat(np.repeat(proj, rep, axis=0), rep, axis=1)[:R, :R]
+        if img.shape[0] < R:
+            idx = (np.arange(R) * N) // R
+            img = proj[np.ix_(idx, idx)]
+        planes[a, :, :, 0] = _encode(np.where(img, 2.0, -14.0), 14.0)
     return planes
 
 
