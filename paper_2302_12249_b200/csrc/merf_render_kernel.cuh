@@ -249,16 +249,13 @@ __device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, i
         blk = bblk;
         if (blk >= 0) {
             const uint2 oct = __ldg(S.vdens + ((size_t)blk * 512 + ((vi[2] & 7) * 8 + (vi[1] & 7)) * 8 + (vi[0] & 7)));
-            const float gx = 1.f - vf[0], gy = 1.f - vf[1], gz = 1.f - vf[2];
-            const float w00 = gy * gz, w10 = vf[1] * gz, w01 = gy * vf[2], w11 = vf[1] * vf[2];
-            s0 = fmaf(gx * w00, byte_f(oct.x, 0), s0);
-            s0 = fmaf(vf[0] * w00, byte_f(oct.x, 1), s0);
-            s0 = fmaf(gx * w10, byte_f(oct.x, 2), s0);
-            s0 = fmaf(vf[0] * w10, byte_f(oct.x, 3), s0);
-            s0 = fmaf(gx * w01, byte_f(oct.y, 0), s0);
-            s0 = fmaf(vf[0] * w01, byte_f(oct.y, 1), s0);
-            s0 = fmaf(gx * w11, byte_f(oct.y, 2), s0);
-            s0 = fmaf(vf[0] * w11, byte_f(oct.y, 3), s0);
+            // trilinear as lerps (corner byte c = dx + 2 dy + 4 dz)
+            const float b0 = byte_f(oct.x, 0), b1 = byte_f(oct.x, 1), b2 = byte_f(oct.x, 2), b3 = byte_f(oct.x, 3);
+            const float b4 = byte_f(oct.y, 0), b5 = byte_f(oct.y, 1), b6 = byte_f(oct.y, 2), b7 = byte_f(oct.y, 3);
+            const float x00 = fmaf(vf[0], b1 - b0, b0), x10 = fmaf(vf[0], b3 - b2, b2);
+            const float x01 = fmaf(vf[0], b5 - b4, b4), x11 = fmaf(vf[0], b7 - b6, b6);
+            const float y0 = fmaf(vf[1], x10 - x00, x00), y1 = fmaf(vf[1], x11 - x01, x01);
+            s0 = fmaf(vf[2], y1 - y0, y0);
         } else {
             n_src -= 1;                    // a missing block contributes nothing
             ret = 2;
@@ -279,11 +276,9 @@ __device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, i
         const int va = (a == 2) ? 1 : 2;
         const uint32_t quad = __ldg(S.pdens + ((size_t)a * S.R + pi[va]) * S.R + pi[ua]);
         const float fu = pf[ua], fv = pf[va];
-        const float gu = 1.f - fu, gv = 1.f - fv;
-        s0 = fmaf(gu * gv, byte_f(quad, 0), s0);
-        s0 = fmaf(fu * gv, byte_f(quad, 1), s0);
-        s0 = fmaf(gu * fv, byte_f(quad, 2), s0);
-        s0 = fmaf(fu * fv, byte_f(quad, 3), s0);
+        const float q0 = byte_f(quad, 0), q1 = byte_f(quad, 1), q2 = byte_f(quad, 2), q3 = byte_f(quad, 3);
+        const float r0 = fmaf(fu, q1 - q0, q0), r1 = fmaf(fu, q3 - q2, q2);
+        s0 += fmaf(fv, r1 - r0, r0);
     }
     const float t0 = fmaf(s0, S.kd, -(float)n_src * S.md);
     const float tau = __expf(t0);
@@ -448,20 +443,26 @@ __global__ void __launch_bounds__(kMarchThreads, 4) march_kernel(DevScene S, int
                 continue;
             }
             if (fcell == last_cell) { found = true; continue; }  // same finest cell: all levels set
+            // finest level first: an occupied finest cell means every coarser (max-pooled) cell
+            // is occupied too, so the sample is evaluated after one probe; only an empty finest
+            // cell searches coarse -> fine for the coarsest empty level, whose cell exit is the
+            // skip target of P:308 (identical result to probing coarse -> fine throughout)
             int e = -1;
+            if (!occ_bit(occ_f, fx, fy, fz, Nf)) {
 #pragma unroll
-            for (int lev = 0; lev < MERF_MAX_LEVELS; lev++) {
-                if (lev < nl && e < 0) {
-                    const int N = S.level_res[lev];
-                    const int sh = S.level_shift[lev];
-                    const int cx = occ_cell(Qx, sh, N), cy = occ_cell(Qy, sh, N), cz = occ_cell(Qz, sh, N);
-                    if (!occ_bit(S.occ[lev], cx, cy, cz, N)) {
-                        // jump to the first lattice sample outside this empty cell (ray-AABB exit)
-                        const int K = qa.w;
-                        e = K;
-                        if (uu.x != 0) e = min(e, exit_axis(qa.x, uu.x, (cx << sh) - kTwoI, ((cx + 1) << sh) - kTwoI, K));
-                        if (uu.y != 0) e = min(e, exit_axis(qa.y, uu.y, (cy << sh) - kTwoI, ((cy + 1) << sh) - kTwoI, K));
-                        if (uu.z != 0) e = min(e, exit_axis(qa.z, uu.z, (cz << sh) - kTwoI, ((cz + 1) << sh) - kTwoI, K));
+                for (int lev = 0; lev < MERF_MAX_LEVELS; lev++) {
+                    if (lev < nl && e < 0) {
+                        const int N = S.level_res[lev];
+                        const int sh = S.level_shift[lev];
+                        const int cx = occ_cell(Qx, sh, N), cy = occ_cell(Qy, sh, N), cz = occ_cell(Qz, sh, N);
+                        if (lev == nl - 1 || !occ_bit(S.occ[lev], cx, cy, cz, N)) {
+                            // jump to the first lattice sample outside this empty cell (ray-AABB exit)
+                            const int K = qa.w;
+                            e = K;
+                            if (uu.x != 0) e = min(e, exit_axis(qa.x, uu.x, (cx << sh) - kTwoI, ((cx + 1) << sh) - kTwoI, K));
+                            if (uu.y != 0) e = min(e, exit_axis(qa.y, uu.y, (cy << sh) - kTwoI, ((cy + 1) << sh) - kTwoI, K));
+                            if (uu.z != 0) e = min(e, exit_axis(qa.z, uu.z, (cz << sh) - kTwoI, ((cz + 1) << sh) - kTwoI, K));
+                        }
                     }
                 }
             }
