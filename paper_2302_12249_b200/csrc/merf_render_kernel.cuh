@@ -360,9 +360,6 @@ __global__ void __launch_bounds__(kMarchThreads, 4) march_kernel(DevScene S, int
     st.cd[0] = st.cd[1] = st.cd[2] = 0.f;
     st.F[0] = st.F[1] = st.F[2] = st.F[3] = 0.f;
     int c_eval = 0, c_donly = 0, c_skip = 0, c_miss = 0;
-    // warp-uniform tile pool [pool_next, pool_end)
-    int pool_next = 0, pool_end = 0;
-    bool exhausted = false;
 
     auto finish = [&]() {
         float4* a = ws.accum + (int64_t)ray * 2;
@@ -373,22 +370,15 @@ __global__ void __launch_bounds__(kMarchThreads, 4) march_kernel(DevScene S, int
     };
 
     while (true) {
-        // ---------------- refill idle lanes from the warp's tile pool ----------------
-        unsigned idle = __ballot_sync(FULL, ray < 0);
-        if (idle != FULL) idle = 0;                       // tile-granular scheduling
-        while (idle && !exhausted) {
-            if (pool_next >= pool_end) {
-                unsigned base = 0;
-                if (lane == 0) base = atomicAdd(ws.queue, 32u);
-                base = __shfl_sync(FULL, base, 0);
-                if ((int64_t)base >= n_rays) { exhausted = true; break; }
-                pool_next = (int)base;
-                pool_end = (int)min((int64_t)base + 32, n_rays);
-            }
-            const int avail = pool_end - pool_next;
-            const int rank = __popc(idle & lt_mask);
-            if (ray < 0 && rank < avail) {
-                ray = pool_next + rank;
+        // ---------------- tile scheduling: a new tile of 32 rays when the warp is empty -------
+        unsigned act = __ballot_sync(FULL, ray >= 0);
+        if (act == 0) {
+            unsigned base = 0;
+            if (lane == 0) base = atomicAdd(ws.queue, 32u);
+            base = __shfl_sync(FULL, base, 0);
+            if ((int64_t)base >= n_rays) break;
+            if ((int64_t)base + lane < n_rays) {
+                ray = (int)base + lane;
                 ns = ws.nseg[ray];
                 j = 0;
                 k = 0;
@@ -405,11 +395,8 @@ __global__ void __launch_bounds__(kMarchThreads, 4) march_kernel(DevScene S, int
                     qa.w = 0;
                 }
             }
-            const int took = min(__popc(idle), avail);
-            pool_next += took;
-            idle = __ballot_sync(FULL, ray < 0);
+            act = __ballot_sync(FULL, ray >= 0);
         }
-        if (__ballot_sync(FULL, ray >= 0) == 0) break;
 
         // ---------------- traversal: advance lanes towards their next evaluated sample ----
         // Warp-synchronous steps; the loop ends as soon as enough lanes hold a sample to shade
@@ -421,7 +408,7 @@ __global__ void __launch_bounds__(kMarchThreads, 4) march_kernel(DevScene S, int
             const bool want = ray >= 0 && !found;
             const unsigned m_want = __ballot_sync(FULL, want);
             if (m_want == 0) break;
-            if (it > 0 && __popc(__ballot_sync(FULL, found)) >= kShadeMin) break;
+            if (it > 0 && __popc(act & ~m_want) >= kShadeMin) break;   // lanes ready to shade
             if (!want) continue;
             if (k >= qa.w) {                                  // segment exhausted
                 j++;
