@@ -255,6 +255,31 @@ merf_status merf_build_occupancy(const uint32_t *finest_bits, const merf_scene_d
 merf_status merf_build_block_index(const uint32_t *finest_bits, const merf_scene_desc *desc,
                                    int32_t *index_out, int64_t *n_blocks, void *stream);
 
+/*
+ * Baking helpers (upstream of the render path).
+ *
+ * merf_bake_occupancy: binary grid A of resolution N from weighted points:
+ * point i (world position x[i], density tau[i], volume-rendering weight w[i]) marks the eight
+ * voxels around its contracted position (cell-centred trilinear corners, clamped; readings
+ * D2, D8, D9) iff w[i] > w_thr and alpha_i = 1 - exp(-tau[i] step) > alpha_thr with the
+ * renderer's step.  The alpha test is evaluated as tau[i] > -ln(1 - alpha_thr)
+ * / step (monotone, exact).  x [device] double [n][3], tau, w [device] double [n];
+ * bits_out [device] uint32 ((N^3+31)/32 words), zeroed by the call.  Asynchronous.
+ * Errors: MERF_EINVAL (N not a power of two in [2, 4096], step <= 0, null pointers).
+ */
+merf_status merf_bake_occupancy(const double *x, const double *tau, const double *w, int64_t n,
+                                int32_t N, double step, double w_thr, double alpha_thr,
+                                uint32_t *bits_out, void *stream);
+
+/*
+ * merf_pack_atlas: block-sparse storage of a dense grid (reading D11): for every stored
+ * block b = index[slot], atlas[b] = dense voxels 8*slot .. 8*slot + 8 per axis (apron clamped
+ * to L - 1).  dense [device] uint8 [L][L][L][8]; index [device] int32 [(L/8)^3];
+ * atlas_out [device] uint8 [n_blocks][9][9][9][8].  Asynchronous.
+ */
+merf_status merf_pack_atlas(const uint8_t *dense, int32_t L, const int32_t *index, int64_t n_blocks,
+                            uint8_t *atlas_out, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -670,3 +670,66 @@ int32_t orc_max_threads(void)
     return 1;
 #endif
 }
+
+/* ---------------------------------------------------------------------------------- */
+/* Baking (NEXT-1).                                                          */
+/* "We mark the eight voxels surrounding a given point x_i as occupied if both the     */
+/* volume rendering weight w_i and the opacity alpha_i exceed a threshold set to 0.005"*/
+/* (P:270), alpha_i = 1 - exp(-tau_i delta) with the renderer's step.       */
+/* The comparison alpha > 0.005 is taken as tau > tau_thr, tau_thr = -ln(1-0.005)/delta */
+/* (monotone; the caller passes tau_thr so both implementations compare the same fp64   */
+/* constant).  Points are world positions, contracted with contract_pi,     */
+/* put on the 2^-F lattice and mapped to the cell-centred grid of resolution N (D9):    */
+/* the eight voxels are the trilinear corners i0, i0 + 1 per axis, clamped to the grid. */
+/* ---------------------------------------------------------------------------------- */
+void orc_bake_occupancy(const double *x, const double *tau, const double *w, int64_t n,
+                        double tau_thr, double w_thr, int32_t N, uint32_t *bits)
+{
+    int64_t words = ((int64_t)N * N * N + 31) / 32;
+    memset(bits, 0, (size_t)words * 4);
+    for (int64_t i = 0; i < n; i++) {
+        if (!(w[i] > w_thr) || !(tau[i] > tau_thr)) continue;
+        double c[3];
+        int g = orc_region_of(x + 3 * i);
+        orc_contract_region(g, x + 3 * i, c);
+        int64_t lo[3], hi[3];
+        for (int a = 0; a < 3; a++) {
+            int64_t Q = llrint(c[a] * (double)ORC_ONE);
+            int64_t i0;
+            double f;
+            texel_coord(Q, N, &i0, &f);
+            lo[a] = i0;
+            hi[a] = i0 + 1;
+        }
+        for (int64_t z = lo[2]; z <= hi[2]; z++)
+            for (int64_t y = lo[1]; y <= hi[1]; y++)
+                for (int64_t xx = lo[0]; xx <= hi[0]; xx++) {
+                    int64_t lin = (z * N + y) * N + xx;
+                    bits[lin >> 5] |= 1u << (lin & 31);
+                }
+    }
+}
+
+/* Block-sparse storage of V (reading D11): block b of the canonical/any index gets
+ * the dense grid's voxels 8b .. 8b+8 per axis (apron clamped to L-1). */
+void orc_pack_atlas(const uint8_t *dense, int32_t L, const int32_t *block_index, int64_t n_blocks,
+                    uint8_t *atlas)
+{
+    int nb = L / 8;
+    for (int64_t slot = 0; slot < (int64_t)nb * nb * nb; slot++) {
+        int32_t b = block_index[slot];
+        if (b < 0 || b >= n_blocks) continue;
+        int bx = (int)(slot % nb), by = (int)((slot / nb) % nb), bz = (int)(slot / ((int64_t)nb * nb));
+        for (int lz = 0; lz < 9; lz++)
+            for (int ly = 0; ly < 9; ly++)
+                for (int lx = 0; lx < 9; lx++) {
+                    int gx = bx * 8 + lx, gy = by * 8 + ly, gz = bz * 8 + lz;
+                    if (gx > L - 1) gx = L - 1;
+                    if (gy > L - 1) gy = L - 1;
+                    if (gz > L - 1) gz = L - 1;
+                    const uint8_t *src = dense + (((size_t)gz * L + gy) * L + gx) * 8;
+                    uint8_t *dst = atlas + (((size_t)b * 9 + lz) * 9 + ly) * 9 * 8 + (size_t)lx * 8;
+                    for (int c = 0; c < 8; c++) dst[c] = src[c];
+                }
+    }
+}

@@ -84,6 +84,8 @@ def lib():
             L.orc_render_rays.argtypes = [vp, vp, vp, vp, i64, C.c_int, C.c_uint32, vp, vp,
                                           i32, vp, vp, vp, vp]
             L.orc_max_threads.restype = i32
+            L.orc_bake_occupancy.argtypes = [vp, vp, vp, i64, dbl, dbl, i32, vp]
+            L.orc_pack_atlas.argtypes = [vp, i32, vp, i64, vp]
             _lib = L
     return _lib
 
@@ -299,3 +301,30 @@ def unpack_trace(cells: np.ndarray):
     return ((cells >> np.uint64(61)).astype(np.int64),
             ((cells >> np.uint64(40)) & np.uint64((1 << 21) - 1)).astype(np.int64),
             (cells & np.uint64((1 << 40) - 1)).astype(np.int64))
+
+
+# ------------------------------------------------------------------------------------
+# baking (NEXT-1)
+# ------------------------------------------------------------------------------------
+def tau_threshold(step: float, alpha_thr: float = 0.005) -> float:
+    """alpha = 1 - exp(-tau step) > alpha_thr  <=>  tau > -ln(1 - alpha_thr) / step."""
+    import math
+    return -math.log1p(-alpha_thr) / step
+
+
+def bake_occupancy(x, tau, w, N: int, step: float, w_thr: float = 0.005, alpha_thr: float = 0.005):
+    x = _c(x, np.float64).reshape(-1, 3)
+    tau = _c(tau, np.float64)
+    w = _c(w, np.float64)
+    bits = np.zeros(n_words(N), np.uint32)
+    lib().orc_bake_occupancy(_p(x), _p(tau), _p(w), len(x), tau_threshold(step, alpha_thr), float(w_thr),
+                             int(N), _p(bits))
+    return bits
+
+
+def pack_atlas(dense, L: int, block_index, n_blocks: int):
+    dense = _c(dense, np.uint8)
+    bi = _c(block_index, np.int32)
+    atlas = np.zeros((n_blocks, 9, 9, 9, 8), np.uint8)
+    lib().orc_pack_atlas(_p(dense), int(L), _p(bi), int(n_blocks), _p(atlas))
+    return atlas

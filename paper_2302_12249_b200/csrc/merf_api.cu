@@ -3,6 +3,7 @@
 // merf_render.cu / merf_build.cu.
 #include <cstdarg>
 #include <cstdio>
+#include <cmath>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -77,7 +78,7 @@ static merf_status validate_desc(const merf_scene_desc* d) {
         return fail(MERF_EINVAL, "n_levels must be in [1, %d]", MERF_MAX_LEVELS);
     for (int i = 0; i < d->n_levels; i++) {
         int N = d->level_res[i];
-        if (!is_pow2(N) || N > 2048) return fail(MERF_EINVAL, "level_res[%d] = %d not a power of two <= 2048", i, N);
+        if (!is_pow2(N) || N > 4096) return fail(MERF_EINVAL, "level_res[%d] = %d not a power of two <= 4096", i, N);
         if (i > 0 && (N % d->level_res[i - 1]) != 0)
             return fail(MERF_EINVAL, "level_res[%d] does not divide level_res[%d]", i - 1, i);
     }
@@ -677,5 +678,25 @@ extern "C" merf_status merf_build_block_index(const uint32_t* finest_bits, const
     CUDA_TRY(cudaStreamSynchronize(st));
     cudaFree(d_need); cudaFree(d_scan); cudaFree(d_count); cudaFree(d_tmp);
     *n_blocks = cnt;
+    return MERF_OK;
+}
+
+extern "C" merf_status merf_bake_occupancy(const double* x, const double* tau, const double* w, int64_t n,
+                                           int32_t N, double step, double w_thr, double alpha_thr,
+                                           uint32_t* bits_out, void* stream) {
+    if (!bits_out || (n > 0 && (!x || !tau || !w))) return fail(MERF_EINVAL, "NULL argument");
+    if (n < 0 || !is_pow2(N) || N < 2 || N > 4096) return fail(MERF_EINVAL, "bad n or N");
+    if (!(step > 0.0) || !(alpha_thr > 0.0 && alpha_thr < 1.0)) return fail(MERF_EINVAL, "bad step / alpha_thr");
+    const double tau_thr = -log1p(-alpha_thr) / step;
+    CUDA_TRY(launch_bake_occupancy(x, tau, w, n, tau_thr, w_thr, N, bits_out, (cudaStream_t)stream));
+    return MERF_OK;
+}
+
+extern "C" merf_status merf_pack_atlas(const uint8_t* dense, int32_t L, const int32_t* index, int64_t n_blocks,
+                                       uint8_t* atlas_out, void* stream) {
+    if (!dense || !index || (!atlas_out && n_blocks > 0)) return fail(MERF_EINVAL, "NULL argument");
+    if (!is_pow2(L) || L < 8 || n_blocks < 0) return fail(MERF_EINVAL, "bad L or n_blocks");
+    if (n_blocks == 0) return MERF_OK;
+    CUDA_TRY(launch_pack_atlas(dense, L, index, n_blocks, atlas_out, (cudaStream_t)stream));
     return MERF_OK;
 }

@@ -154,6 +154,51 @@ __global__ void pack_voxel_density_kernel(const uint8_t* __restrict__ atlas, int
     vdens[i] = make_uint2(w[0], w[1]);
 }
 
+// NEXT-1 baking: one thread per weighted point; a point with w > w_thr and
+// tau > tau_thr (i.e. alpha = 1 - exp(-tau Delta) > 0.005 with the renderer's step)
+// marks the eight voxels around its contracted position (trilinear corners of the
+// cell-centred grid, reading D9) with atomicOr.  Contraction in canonical fp64 (D8).
+__global__ void bake_occupancy_kernel(const double* __restrict__ x, const double* __restrict__ tau,
+                                      const double* __restrict__ w, int64_t n, double tau_thr,
+                                      double w_thr, int N, uint32_t* __restrict__ bits) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (!(w[i] > w_thr) || !(tau[i] > tau_thr)) return;
+    const double p[3] = {x[3 * i], x[3 * i + 1], x[3 * i + 2]};
+    double c[3];
+    contract_region(region_of(p[0], p[1], p[2]), p, c);
+    const int s = kF + 2 - ilog2(N);
+    int lo[3];
+#pragma unroll
+    for (int a = 0; a < 3; a++) lo[a] = base_voxel(__double2ll_rn(mul_rn(c[a], (double)kOne)), s, N);
+#pragma unroll
+    for (int cz = 0; cz < 2; cz++)
+#pragma unroll
+        for (int cy = 0; cy < 2; cy++)
+#pragma unroll
+            for (int cx = 0; cx < 2; cx++) {
+                const int64_t lin = ((int64_t)(lo[2] + cz) * N + (lo[1] + cy)) * N + (lo[0] + cx);
+                atomicOr(bits + (lin >> 5), 1u << (lin & 31));
+            }
+}
+
+// Block-sparse storage of a dense V (D11): one thread per (block, voxel of 9^3).
+__global__ void pack_atlas_kernel(const uint8_t* __restrict__ dense, int L, const int32_t* __restrict__ index,
+                                  int64_t n_slots, int64_t n_blocks, uint8_t* __restrict__ atlas) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_slots * 729) return;
+    const int64_t slot = i / 729;
+    const int l = (int)(i - slot * 729);
+    const int32_t b = index[slot];
+    if (b < 0 || b >= n_blocks) return;
+    const int nb = L / 8;
+    const int bx = (int)(slot % nb), by = (int)((slot / nb) % nb), bz = (int)(slot / ((int64_t)nb * nb));
+    const int lx = l % 9, ly = (l / 9) % 9, lz = l / 81;
+    const int gx = min(bx * 8 + lx, L - 1), gy = min(by * 8 + ly, L - 1), gz = min(bz * 8 + lz, L - 1);
+    const uint2 v = *reinterpret_cast<const uint2*>(dense + (((size_t)gz * L + gy) * L + gx) * 8);
+    *reinterpret_cast<uint2*>(atlas + ((size_t)b * 729 + l) * 8) = v;
+}
+
 static inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 cudaError_t launch_maxpool_bits(const uint32_t* fine, int f, uint32_t* coarse, int N, cudaStream_t st) {
@@ -198,6 +243,21 @@ cudaError_t launch_pack_density(const uint8_t* planes, int R, uint32_t* pdens, c
         pack_plane_density_kernel<<<blocks_for((int64_t)3 * R * R, 256), 256, 0, st>>>(planes, R, pdens);
     if (atlas && n_blocks > 0)
         pack_voxel_density_kernel<<<blocks_for(n_blocks * 512, 256), 256, 0, st>>>(atlas, n_blocks, vdens);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bake_occupancy(const double* x, const double* tau, const double* w, int64_t n,
+                                  double tau_thr, double w_thr, int N, uint32_t* bits, cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(bits, 0, (size_t)(((int64_t)N * N * N + 31) / 32) * 4, st);
+    if (e != cudaSuccess || n <= 0) return e;
+    bake_occupancy_kernel<<<blocks_for(n, 256), 256, 0, st>>>(x, tau, w, n, tau_thr, w_thr, N, bits);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pack_atlas(const uint8_t* dense, int L, const int32_t* index, int64_t n_blocks,
+                              uint8_t* atlas, cudaStream_t st) {
+    const int64_t slots = (int64_t)(L / 8) * (L / 8) * (L / 8);
+    pack_atlas_kernel<<<blocks_for(slots * 729, 256), 256, 0, st>>>(dense, L, index, slots, n_blocks, atlas);
     return cudaGetLastError();
 }
 

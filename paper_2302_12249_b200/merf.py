@@ -89,6 +89,8 @@ SIGNATURES = [
     ("merf_segments", C.c_int, [_vp, C.POINTER(merf_camera), _i32, _vp, _i64, _i32, _vp, _vp, _vp]),
     ("merf_contract", C.c_int, [_vp, _i64, _vp, _vp, _vp]),
     ("merf_build_occupancy", C.c_int, [_vp, C.POINTER(merf_scene_desc), _vp, _vp]),
+    ("merf_bake_occupancy", C.c_int, [_vp, _vp, _vp, _i64, _i32, C.c_double, C.c_double, C.c_double, _vp, _vp]),
+    ("merf_pack_atlas", C.c_int, [_vp, _i32, _vp, _i64, _vp, _vp]),
     ("merf_build_block_index", C.c_int, [_vp, C.POINTER(merf_scene_desc), _vp, C.POINTER(_i64), _vp]),
 ]
 
@@ -267,6 +269,18 @@ def merf_build_block_index(finest_bits, scene, index_out, stream=None) -> int:
     _check(lib().merf_build_block_index(_ptr(finest_bits), C.byref(desc), _ptr(index_out), C.byref(n),
                                         _stream(stream)))
     return int(n.value)
+
+
+def merf_bake_occupancy(x, tau, w, N: int, step: float, bits_out, w_thr: float = 0.005,
+                        alpha_thr: float = 0.005, stream=None) -> None:
+    """A from weighted points; x [n,3] / tau / w float64 device tensors."""
+    _check(lib().merf_bake_occupancy(_ptr(x), _ptr(tau), _ptr(w), int(x.shape[0]), int(N), float(step),
+                                     float(w_thr), float(alpha_thr), _ptr(bits_out), _stream(stream)))
+
+
+def merf_pack_atlas(dense, L: int, index, n_blocks: int, atlas_out, stream=None) -> None:
+    _check(lib().merf_pack_atlas(_ptr(dense), int(L), _ptr(index), int(n_blocks), _ptr(atlas_out),
+                                 _stream(stream)))
 
 
 class Scene:
