@@ -4,6 +4,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -179,6 +180,9 @@ extern "C" merf_status merf_scene_upload(const merf_scene_desc* desc, const uint
 #define UPC_TRY(expr) do { cudaError_t _e = (expr); if (_e != cudaSuccess) \
         return bail(fail(_e == cudaErrorMemoryAllocation ? MERF_ENOMEM : MERF_ECUDA, "%s: %s", #expr, cudaGetErrorString(_e))); } while (0)
 
+    // Every upload step (host->device copies included) is ordered on this one stream:
+    // a blocking cudaMemcpy from pageable memory may return before its DMA lands, so a
+    // kernel on another stream could read stale device memory.
     cudaStream_t cs;
     UPC_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
     {   // keep render workspaces cached in the stream-ordered pool between calls
@@ -191,7 +195,7 @@ extern "C" merf_status merf_scene_upload(const merf_scene_desc* desc, const uint
     // ---- MLP weights
     float* d_mlp;
     UP_TRY(dalloc(s, &d_mlp, kMlpFloats * sizeof(float)));
-    UPC_TRY(cudaMemcpy(d_mlp, mlp, kMlpFloats * sizeof(float), cudaMemcpyHostToDevice));
+    UPC_TRY(cudaMemcpyAsync(d_mlp, mlp, kMlpFloats * sizeof(float), cudaMemcpyHostToDevice, cs));
     S.mlp = d_mlp;
     // ---- planes
     if (use_p) {
@@ -199,8 +203,8 @@ extern "C" merf_status merf_scene_upload(const merf_scene_desc* desc, const uint
         uint8_t* d_pl;
         // padded by one texel row: the clamped upper-edge corner (weight 0) stays in bounds
         UP_TRY(dalloc(s, &d_pl, pb + (size_t)(desc->R + 2) * 8));
-        UPC_TRY(cudaMemset(d_pl + pb, 0, (size_t)(desc->R + 2) * 8));
-        UPC_TRY(cudaMemcpy(d_pl, planes, pb, cudaMemcpyHostToDevice));
+        UPC_TRY(cudaMemsetAsync(d_pl + pb, 0, (size_t)(desc->R + 2) * 8, cs));
+        UPC_TRY(cudaMemcpyAsync(d_pl, planes, pb, cudaMemcpyHostToDevice, cs));
         S.planes = d_pl;
         uint32_t* d_pd;
         UP_TRY(dalloc(s, &d_pd, (size_t)3 * desc->R * desc->R * 4));
@@ -212,9 +216,9 @@ extern "C" merf_status merf_scene_upload(const merf_scene_desc* desc, const uint
     const int Nf = desc->level_res[nl - 1];
     uint32_t* d_occ[MERF_MAX_LEVELS] = {nullptr, nullptr, nullptr, nullptr};
     for (int i = 0; i < nl; i++) UP_TRY(dalloc(s, &d_occ[i], occ_words(desc->level_res[i]) * 4));
-    UPC_TRY(cudaMemcpy(d_occ[nl - 1], occ_finest, occ_words(Nf) * 4, cudaMemcpyHostToDevice));
-    for (int i = 0; i < nl - 1; i++)
-        UPC_TRY(launch_maxpool_bits(d_occ[nl - 1], Nf, d_occ[i], desc->level_res[i], cs));
+    UPC_TRY(cudaMemcpyAsync(d_occ[nl - 1], occ_finest, occ_words(Nf) * 4, cudaMemcpyHostToDevice, cs));
+    for (int i = nl - 2; i >= 0; i--)       // each level from the next finer one (nested)
+        UPC_TRY(launch_maxpool_bits(d_occ[i + 1], desc->level_res[i + 1], d_occ[i], desc->level_res[i], cs));
     for (int i = 0; i < MERF_MAX_LEVELS; i++) S.occ[i] = d_occ[i < nl ? i : nl - 1];
     // ---- block index (K1) + atlas
     if (use_v) {
@@ -236,7 +240,7 @@ extern "C" merf_status merf_scene_upload(const merf_scene_desc* desc, const uint
         UPC_TRY(launch_block_need(d_occ[nl - 1], Nf, desc->L, d_need, cs));
         int64_t canon = 0;
         if (block_index) {
-            UPC_TRY(cudaMemcpy(d_idx, block_index, slots * 4, cudaMemcpyHostToDevice));
+            UPC_TRY(cudaMemcpyAsync(d_idx, block_index, slots * 4, cudaMemcpyHostToDevice, cs));
             int32_t* d_canon;
             UPC_TRY(cudaMalloc(&d_canon, slots * 4));
             UPC_TRY(launch_block_number(d_need, slots, d_canon, d_count, d_tmp, &tb, d_scan, cs));
@@ -262,7 +266,7 @@ extern "C" merf_status merf_scene_upload(const merf_scene_desc* desc, const uint
         size_t ab = (size_t)n_blocks * 729 * 8;
         uint8_t* d_at;
         UP_TRY(dalloc(s, &d_at, ab));
-        if (ab) UPC_TRY(cudaMemcpy(d_at, atlas, ab, cudaMemcpyHostToDevice));
+        if (ab) UPC_TRY(cudaMemcpyAsync(d_at, atlas, ab, cudaMemcpyHostToDevice, cs));
         S.block_index = d_idx;
         S.atlas = d_at;
         uint2* d_vd;
@@ -348,6 +352,8 @@ static merf_status ws_alloc(int64_t n, cudaStream_t st, Workspace& ws, void** ba
     const size_t ns = align256((size_t)n);
     const size_t acc = align256((size_t)n * 32);
     CUDA_TRY(cudaMallocAsync(base, seg + ns + acc + 256, st));
+    static const bool poison = getenv("MERF_DEBUG_POISON") != nullptr;   // debug: NaN-fill
+    if (poison) CUDA_TRY(cudaMemsetAsync(*base, 0xFF, seg + ns + acc + 256, st));
     char* b = (char*)*base;
     ws.seg = (int4*)b;
     ws.nseg = (uint8_t*)(b + seg);
@@ -643,11 +649,15 @@ extern "C" merf_status merf_build_occupancy(const uint32_t* finest_bits, const m
     merf_status e = validate_desc(desc);
     if (e) return e;
     if (!finest_bits || (!levels_out && desc->n_levels > 1)) return fail(MERF_EINVAL, "NULL argument");
-    const int nl = desc->n_levels, Nf = desc->level_res[nl - 1];
-    uint32_t* o = levels_out;
-    for (int i = 0; i < nl - 1; i++) {
-        CUDA_TRY(launch_maxpool_bits(finest_bits, Nf, o, desc->level_res[i], (cudaStream_t)stream));
-        o += occ_words(desc->level_res[i]);
+    const int nl = desc->n_levels;
+    // offsets of the coarser levels in levels_out (coarse -> fine), built fine -> coarse, each
+    // from the next finer one (levels are nested: each divides the next)
+    int64_t off[MERF_MAX_LEVELS] = {0, 0, 0, 0};
+    for (int i = 1; i < nl - 1; i++) off[i] = off[i - 1] + occ_words(desc->level_res[i - 1]);
+    for (int i = nl - 2; i >= 0; i--) {
+        const uint32_t* src = (i == nl - 2) ? finest_bits : levels_out + off[i + 1];
+        CUDA_TRY(launch_maxpool_bits(src, desc->level_res[i + 1], levels_out + off[i], desc->level_res[i],
+                                     (cudaStream_t)stream));
     }
     return MERF_OK;
 }

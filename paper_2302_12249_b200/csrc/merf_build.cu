@@ -51,6 +51,44 @@ __global__ void maxpool_bits_kernel(const uint32_t* __restrict__ fine, int f,
     coarse[word] = out;
 }
 
+// OR-pool by 2 in x, y and z (fine resolution 2N, N >= 32): one thread per coarse 32-bit
+// word = 32 coarse cells of one (z, y) row; it reads the 2 x 2 rows of 2 fine words,
+// ORs them, ORs adjacent bit pairs and compacts the even bits.  Every fine word is read
+// exactly once (bandwidth-bound); repeated halvings give the max-pool of any power-of-two
+// factor exactly (OR is associative).
+__device__ __forceinline__ uint32_t compact_even(uint32_t x) {
+    x &= 0x55555555u;
+    x = (x | (x >> 1)) & 0x33333333u;
+    x = (x | (x >> 2)) & 0x0F0F0F0Fu;
+    x = (x | (x >> 4)) & 0x00FF00FFu;
+    x = (x | (x >> 8)) & 0x0000FFFFu;
+    return x;
+}
+
+__global__ void halve_bits_kernel(const uint32_t* __restrict__ fine, uint32_t* __restrict__ coarse, int N) {
+    const int64_t words = (int64_t)N * N * N / 32;
+    const int64_t wi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (wi >= words) return;
+    const int wpr = N / 32;                          // coarse words per row
+    const int wx = (int)(wi % wpr);
+    const int64_t row = wi / wpr;                    // z * N + y
+    const int y = (int)(row % N), z = (int)(row / N);
+    const int F = 2 * N, fwpr = F / 32;
+    uint32_t lo = 0, hi = 0;
+#pragma unroll
+    for (int dz = 0; dz < 2; dz++)
+#pragma unroll
+        for (int dy = 0; dy < 2; dy++) {
+            const int64_t frow = (int64_t)(2 * z + dz) * F + (2 * y + dy);
+            const uint32_t* p = fine + frow * fwpr + 2 * wx;
+            lo |= __ldg(p);
+            hi |= __ldg(p + 1);
+        }
+    lo |= lo >> 1;
+    hi |= hi >> 1;
+    coarse[wi] = compact_even(lo) | (compact_even(hi) << 16);
+}
+
 // Lower trilinear base voxel of lattice coordinate Q on the L grid (clamped, as the render
 // kernel's texel()).
 __device__ __forceinline__ int base_voxel(int64_t Q, int s, int L) {
@@ -202,9 +240,39 @@ __global__ void pack_atlas_kernel(const uint8_t* __restrict__ dense, int L, cons
 static inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 cudaError_t launch_maxpool_bits(const uint32_t* fine, int f, uint32_t* coarse, int N, cudaStream_t st) {
-    int64_t words = ((int64_t)N * N * N + 31) / 32;
-    maxpool_bits_kernel<<<blocks_for(words, 256), 256, 0, st>>>(fine, f, coarse, N);
-    return cudaGetLastError();
+    if (N < 32 || f / N <= 2) {                      // small levels / single halving: direct
+        if (N >= 32 && f == 2 * N) {
+            halve_bits_kernel<<<blocks_for((int64_t)N * N * N / 32, 256), 256, 0, st>>>(fine, coarse, N);
+            return cudaGetLastError();
+        }
+        int64_t words = ((int64_t)N * N * N + 31) / 32;
+        maxpool_bits_kernel<<<blocks_for(words, 256), 256, 0, st>>>(fine, f, coarse, N);
+        return cudaGetLastError();
+    }
+    // successive halvings f -> f/2 -> ... -> N through stream-ordered temporaries
+    const uint32_t* src = fine;
+    uint32_t* tmp[2] = {nullptr, nullptr};
+    int cur = f, t = 0;
+    cudaError_t e = cudaSuccess;
+    while (cur / 2 > N) {
+        const int n2 = cur / 2;
+        const size_t bytes = (size_t)n2 * n2 * n2 / 8;
+        if (tmp[t] == nullptr && (e = cudaMallocAsync(&tmp[t], (size_t)(cur / 2) * (cur / 2) * (cur / 2) / 8, st)) != cudaSuccess)
+            break;
+        (void)bytes;
+        halve_bits_kernel<<<blocks_for((int64_t)n2 * n2 * n2 / 32, 256), 256, 0, st>>>(src, tmp[t], n2);
+        src = tmp[t];
+        t ^= 1;
+        if (tmp[t]) { cudaFreeAsync(tmp[t], st); tmp[t] = nullptr; }
+        cur = n2;
+    }
+    if (e == cudaSuccess) {
+        halve_bits_kernel<<<blocks_for((int64_t)N * N * N / 32, 256), 256, 0, st>>>(src, coarse, N);
+        e = cudaGetLastError();
+    }
+    for (int i = 0; i < 2; i++)
+        if (tmp[i]) cudaFreeAsync(tmp[i], st);
+    return e;
 }
 
 cudaError_t launch_block_need(const uint32_t* finest, int N, int L, uint8_t* need, cudaStream_t st) {

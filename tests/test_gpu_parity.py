@@ -390,3 +390,23 @@ def test_segments_bit_exact(M, c1_scene, cfg):
             assert a["region"] == b["region"] and a["K"] == b["K"], p
             assert a["t_a"] == b["t_a"] and (a["t_b"] == b["t_b"]), p
             assert np.array_equal(a["Qa"], b["Qa"]) and np.array_equal(a["U"], b["U"]), p
+
+
+def test_upload_copies_inputs_before_returning(M):
+    """Regression (stale-upload bug): the render after an upload must see exactly the uploaded
+    arrays even if the caller overwrites its host buffers right after merf_scene_upload
+    returns (ownership contract in include/merf.h)."""
+    import copy
+    import torch
+    sc = random_scene(seed=8, L=64, R=64, level_res=(8, 32), occ_fraction=0.3)
+    ref_sc = copy.deepcopy(sc)
+    s = M.Scene(sc)
+    sc.atlas[...] = 255
+    sc.planes[...] = 255
+    sc.occ_finest[...] = 0
+    cams, W, H = config_cameras("c1")
+    out = s.render(cams, W, H)
+    torch.cuda.synchronize()
+    ref = O.render(O.OracleScene(ref_sc), cams[0], W, H)
+    assert np.abs(out[0].reshape(-1, 3).cpu().numpy() - ref["rgb"]).max() <= TOL
+    s.close()

@@ -49,8 +49,7 @@ def main():
     for N in (256, 4096):
         bits = torch.empty((N ** 3 + 31) // 32, dtype=torch.int32, device="cuda")
         ms = timed(lambda: M.merf_bake_occupancy(x, tau, w, N, 2.0 ** -10, bits))
-        out.append(dict(op="bake_occupancy", N=N, points=n, ms=ms, points_per_s=n / (ms / 1e3),
-                        occupied=int(torch.sum(torch.bitwise_count(bits) if hasattr(torch, "bitwise_count") else 0))))
+        out.append(dict(op="bake_occupancy", N=N, points=n, ms=ms, points_per_s=n / (ms / 1e3)))
     desc = MerfScene(L=512, R=2048, level_res=(32, 128, 256, 4096), step=2.0 ** -10,
                      planes=np.zeros(1, np.uint8), block_index=np.zeros(1, np.int32),
                      atlas=np.zeros((0, 9, 9, 9, 8), np.uint8), occ_finest=np.zeros(1, np.uint32),
