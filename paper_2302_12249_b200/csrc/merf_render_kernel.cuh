@@ -43,6 +43,7 @@ constexpr int kMarchThreads = 256;
 // hold a sample or after kTravSteps steps.
 constexpr int kShadeMin = 16;
 constexpr int kTravSteps = 16;
+struct MarchTune { int shade_min, trav_steps; };   // runtime override (MERF_TUNE="shade,steps")
 
 // ------------------------------------------------------------------------------------
 // ray indexing: camera rays are numbered in 8x4-pixel tile order (32 rays per tile, one
@@ -340,7 +341,7 @@ __device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, i
 template <int KF>
 __global__ void __launch_bounds__(kMarchThreads, 4) march_kernel(DevScene S, int64_t n_rays, Workspace ws,
                                                               uint32_t rflags, TraceArgs ta,
-                                                              unsigned long long* stats) {
+                                                              unsigned long long* stats, MarchTune tune) {
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
@@ -404,11 +405,11 @@ __global__ void __launch_bounds__(kMarchThreads, 4) march_kernel(DevScene S, int
         // skip chain never idles the rest of the warp.
         bool found = false;
         int Qx = 0, Qy = 0, Qz = 0, fcell = 0;
-        for (int it = 0; it < kTravSteps; it++) {
+        for (int it = 0; it < tune.trav_steps; it++) {
             const bool want = ray >= 0 && !found;
             const unsigned m_want = __ballot_sync(FULL, want);
             if (m_want == 0) break;
-            if (it > 0 && __popc(act & ~m_want) >= kShadeMin) break;   // lanes ready to shade
+            if (it > 0 && __popc(act & ~m_want) >= tune.shade_min) break;   // lanes ready to shade
             if (!want) continue;
             if (k >= qa.w) {                                  // segment exhausted
                 j++;
