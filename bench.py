@@ -164,7 +164,7 @@ def run_reference(args):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "orbit1080p_paper_scale_merf", "scene": "c2 (512^3 sparse grid, 3x2048^2 planes)",
+            "config": {"workload": "orbit1080p_paper_scale_merf" + ("_dense_ablation" if args.dense else ""), "scene": "c2 (512^3 sparse grid, 3x2048^2 planes)",
                        "sample": f"every {stride}th pixel of one 1920x1080 orbit view per step"},
             "cpu_baseline": {"value": value, "unit": "rays/s", "cores": O.max_threads(), "kind": "oracle",
                              "sample": f"every {stride}th pixel of one 1920x1080 orbit view per step"},
@@ -183,6 +183,8 @@ def main():
     ap.add_argument("--views", type=int, default=16, help="views per rank per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dense", action="store_true",
+                    help="ablation: dense lattice stepping gated by the finest level (no skipping)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -209,6 +211,7 @@ def main():
     steps_total = args.warmup + args.steps
     batches = [orbit_cameras(N_ORBIT, indices=views_for(rank, world, s, V)) for s in range(steps_total)]
 
+    extra_flags = M.MERF_DENSE if args.dense else 0
     stream = torch.cuda.Stream()
     gstream = torch.cuda.Stream()
     frames = [torch.empty((V, H_IMG, W_IMG, 4), dtype=torch.uint8, device=dev) for _ in range(2)]
@@ -218,7 +221,7 @@ def main():
     with torch.cuda.stream(stream):
         for s in range(args.warmup, steps_total):
             st = M.merf_render(scene.handle, batches[s], W_IMG, H_IMG, frames[0], fmt=M.MERF_RGBA_U8,
-                               stream=stream, stats=True)
+                               flags=extra_flags, stream=stream, stats=True)
             app = st["evaluated"] - st["density_only"]
             algo_bytes.append(BYTES_APPEARANCE * app + BYTES_DENSITY_ONLY * st["density_only"])
             n_eval += st["evaluated"]
@@ -234,7 +237,7 @@ def main():
                 stream.wait_stream(gstream)          # buffer reuse after its gather
             ev0[s].record(stream)
             M.merf_render(scene.handle, batches[s], W_IMG, H_IMG, buf, fmt=M.MERF_RGBA_U8,
-                          flags=M.MERF_TIMED if s >= args.warmup else 0, stream=stream)
+                          flags=(M.MERF_TIMED if s >= args.warmup else 0) | extra_flags, stream=stream)
             ev1[s].record(stream)
         if world > 1:
             gstream.wait_stream(stream)
@@ -326,7 +329,7 @@ def main():
             "metric": METRIC, "value": value, "unit": "rays/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "orbit1080p_paper_scale_merf",
+            "config": {"workload": "orbit1080p_paper_scale_merf" + ("_dense_ablation" if args.dense else ""),
                        "views_per_rank_per_step": V, "W": W_IMG, "H": H_IMG,
                        "scene": {k: info[k] for k in ("L", "R", "level_res", "n_blocks", "device_bytes")},
                        "block_fraction": info["n_blocks"] / (info["L"] // 8) ** 3 if info["L"] else None,
