@@ -410,3 +410,47 @@ def test_upload_copies_inputs_before_returning(M):
     ref = O.render(O.OracleScene(ref_sc), cams[0], W, H)
     assert np.abs(out[0].reshape(-1, 3).cpu().numpy() - ref["rgb"]).max() <= TOL
     s.close()
+
+
+def test_bench_launch_configuration(M, c2):
+    """The exact launch bench.py times: 16 orbit views at 1920x1080 in one merf_render call
+    (two 8-view chunks of the persistent pipeline), RGBA8 output, MERF_TIMED.  Sampled pixels
+    of four views vs the oracle: |u8 - round(255 C_oracle)| <= 1."""
+    import torch
+    import bench
+    cams = orbit_cameras(256, indices=bench.views_for(0, 1, 3, 16))
+    s = M.Scene(c2)
+    out = torch.empty((16, 1080, 1920, 4), dtype=torch.uint8, device="cuda")
+    M.merf_render(s.handle, cams, 1920, 1080, out, fmt=M.MERF_RGBA_U8, flags=M.MERF_TIMED)
+    torch.cuda.synchronize()
+    kt = M.merf_kernel_times_get(s.handle)
+    assert kt["march_launches"] == 2 and kt["setup_launches"] == 2 and kt["shade_launches"] == 2
+    osc = O.OracleScene(c2)
+    rng = np.random.default_rng(11)
+    for v in (0, 7, 8, 15):                      # both chunks, first and last views
+        pix = rng.integers(0, 1920 * 1080, 1500)
+        ref = O.render(osc, cams[v], 1920, 1080, pixels=pix)["rgb"]
+        got = out[v].reshape(-1, 4)[torch.as_tensor(pix, device="cuda")].cpu().numpy()
+        assert (got[:, 3] == 255).all()
+        assert np.abs(got[:, :3].astype(int) - np.rint(ref * 255).astype(int)).max() <= 1, v
+    s.close()
+
+
+def test_render_argument_errors(M, c1_scene):
+    import torch
+    s = M.Scene(c1_scene)
+    cams, W, H = config_cameras("c1")
+    out = torch.empty((1, H, W, 3), device="cuda")
+    for bad in (dict(W=0), dict(H=-1), dict(fmt=7)):
+        kw = dict(W=W, H=H, fmt=M.MERF_RGB_F32)
+        kw.update(bad)
+        with pytest.raises(M.MerfError) as e:
+            M.merf_render(s.handle, cams, kw["W"], kw["H"], out, fmt=kw["fmt"])
+        assert e.value.status == M.MERF_EINVAL
+    with pytest.raises(M.MerfError):
+        M.merf_render(s.handle, cams, 70000, 70000, out)            # W*H overflow
+    bad_cam = cams.copy()
+    bad_cam[0, 12] = 0.0                                            # fx = 0
+    with pytest.raises(M.MerfError):
+        M.merf_render(s.handle, bad_cam, W, H, out)
+    s.close()
