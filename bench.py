@@ -164,7 +164,8 @@ def run_reference(args):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "orbit1080p_paper_scale_merf" + ("_dense_ablation" if args.dense else ""), "scene": "c2 (512^3 sparse grid, 3x2048^2 planes)",
+            "config": {"workload": "orbit1080p_paper_scale_merf" + ("_dense_ablation" if args.dense else "")
+                                   + ("_spherical_contraction" if args.spherical else ""), "scene": "c2 (512^3 sparse grid, 3x2048^2 planes)",
                        "sample": f"every {stride}th pixel of one 1920x1080 orbit view per step"},
             "cpu_baseline": {"value": value, "unit": "rays/s", "cores": O.max_threads(), "kind": "oracle",
                              "sample": f"every {stride}th pixel of one 1920x1080 orbit view per step"},
@@ -183,6 +184,9 @@ def main():
     ap.add_argument("--views", type=int, default=16, help="views per rank per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--spherical", action="store_true",
+                    help="NEXT-2 comparison: the scene baked in the spherical contraction's space, "
+                         "rendered with fixed contracted-arc-length steps and no AABB skipping")
     ap.add_argument("--dense", action="store_true",
                     help="ablation: dense lattice stepping gated by the finest level (no skipping)")
     args = ap.parse_args()
@@ -204,14 +208,14 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = f"cuda:{local}"
 
-    sc = make_scene("c2")
+    sc = make_scene("c2", contraction="sph" if args.spherical else "pi")
     scene = M.Scene(sc, device=local)
     info = scene.info()
     V = args.views
     steps_total = args.warmup + args.steps
     batches = [orbit_cameras(N_ORBIT, indices=views_for(rank, world, s, V)) for s in range(steps_total)]
 
-    extra_flags = M.MERF_DENSE if args.dense else 0
+    extra_flags = (M.MERF_DENSE if args.dense else 0) | (M.MERF_SPHERICAL if args.spherical else 0)
     stream = torch.cuda.Stream()
     gstream = torch.cuda.Stream()
     frames = [torch.empty((V, H_IMG, W_IMG, 4), dtype=torch.uint8, device=dev) for _ in range(2)]
@@ -329,7 +333,8 @@ def main():
             "metric": METRIC, "value": value, "unit": "rays/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "orbit1080p_paper_scale_merf" + ("_dense_ablation" if args.dense else ""),
+            "config": {"workload": "orbit1080p_paper_scale_merf" + ("_dense_ablation" if args.dense else "")
+                                   + ("_spherical_contraction" if args.spherical else ""),
                        "views_per_rank_per_step": V, "W": W_IMG, "H": H_IMG,
                        "scene": {k: info[k] for k in ("L", "R", "level_res", "n_blocks", "device_bytes")},
                        "block_fraction": info["n_blocks"] / (info["L"] // 8) ** 3 if info["L"] else None,

@@ -66,7 +66,13 @@ enum {
     MERF_NO_EARLY_TERM = 1u,   /* disable termination at T < t_min                */
     MERF_COUNTERS = 2u,        /* accumulate merf_stats (adds device atomics)             */
     MERF_DENSE = 4u,           /* debug: dense stepping gated by the finest level only     */
-    MERF_TIMED = 8u            /* record CUDA events around every pipeline kernel launch     */
+    MERF_TIMED = 8u,           /* record CUDA events around every pipeline kernel launch     */
+    MERF_SPHERICAL = 16u       /* NEXT-2 comparison variant: the scene's grids live in the
+                                  space of the spherical contraction of Eq. 4;
+                                  fixed contracted-arc-length Euler steps, t += Delta/sigma(t),
+                                  every sample tested against the finest level, no AABB skip
+                                  (P:222-226).  Accepted by merf_render, merf_render_rays,
+                                  merf_trace (segment ordinal 0, k = step index).            */
 };
 
 #define MERF_MAX_LEVELS 4

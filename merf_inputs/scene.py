@@ -236,9 +236,37 @@ def _inverse_contract(c):
     return x, outer, j, sj, scale
 
 
+def _contracted_distance_sph(world: World, c: np.ndarray, chunk: int = 1 << 19):
+    """as contracted_distance, for the spherical contraction of Eq. 4 (NEXT-2 scenes):
+    x = r(rho) c/rho with rho = |c|, r = 1/(2 - rho) outside the unit ball, so
+    grad_c f = r^2 (g.c^) c^ + (r / rho) (g - (g.c^) c^)."""
+    import torch
+    out_d = np.empty(len(c))
+    out_id = np.empty(len(c), np.int64)
+    for s in range(0, len(c), chunk):
+        cc = torch.from_numpy(np.ascontiguousarray(c[s:s + chunk], np.float64))
+        rho = torch.sqrt((cc * cc).sum(1)).clamp_min(1e-12)
+        outer = rho > 1.0
+        r = torch.where(outer, 1.0 / (2.0 - rho).clamp_min(1e-9), rho)
+        ch = cc / rho[:, None]
+        x = torch.where(outer[:, None], ch * r[:, None], cc)
+        f, g, oid = world.sdf(x)
+        gr = (g * ch).sum(1)
+        gc = torch.where(outer[:, None], (r * r * gr)[:, None] * ch + (r / rho)[:, None] * (g - gr[:, None] * ch), g)
+        nrm = torch.sqrt((gc * gc).sum(1)).clamp_min(1e-30)
+        out_d[s:s + chunk] = (f / nrm).numpy()
+        out_id[s:s + chunk] = oid.numpy()
+    return out_d, out_id
+
+
+_CONTRACTION = ["pi"]     # contraction the generator bakes for (make_scene(contraction=...))
+
+
 def contracted_distance(world: World, c: np.ndarray, chunk: int = 1 << 19):
     """first-order contracted-space signed distance, object id at contracted points."""
     import torch
+    if _CONTRACTION[0] == "sph":
+        return _contracted_distance_sph(world, c, chunk)
     out_d = np.empty(len(c))
     out_id = np.empty(len(c), np.int64)
     for s in range(0, len(c), chunk):
@@ -258,7 +286,10 @@ def contracted_distance(world: World, c: np.ndarray, chunk: int = 1 << 19):
 
 
 def _reachable(c: np.ndarray) -> np.ndarray:
-    """contracted points with at most one |c_j| > 1 (the image of contract_pi is cross-shaped)."""
+    """contracted points in the image of the contraction: at most one |c_j| > 1 for contract_pi
+    (cross-shaped image), |c| < 2 for the spherical contraction."""
+    if _CONTRACTION[0] == "sph":
+        return np.sqrt((c * c).sum(axis=1)) < 2.0
     return (np.abs(c) > 1.0).sum(axis=1) <= 1
 
 
@@ -310,8 +341,20 @@ CONFIGS = {
 
 def make_scene(config: str = "c1", seed: int = SEED, L=None, R=None, level_res=None, step=None,
                band_cells: float = 1.25, ramp_cells: float = 0.5, density_bias: float = 0.0,
-               source_mask: int = 15, mlp_scale: float = 0.3) -> MerfScene:
-    """The synthetic world baked at (L, R, levels).  c2/c3/c4 share the paper-scale scene."""
+               source_mask: int = 15, mlp_scale: float = 0.3, contraction: str = "pi") -> MerfScene:
+    """The synthetic world baked at (L, R, levels).  c2/c3/c4 share the paper-scale scene.
+    contraction="sph" bakes the same world in the spherical contraction's space (NEXT-2)."""
+    assert contraction in ("pi", "sph")
+    _CONTRACTION[0] = contraction
+    try:
+        return _make_scene(config, seed, L, R, level_res, step, band_cells, ramp_cells, density_bias,
+                           source_mask, mlp_scale, contraction)
+    finally:
+        _CONTRACTION[0] = "pi"
+
+
+def _make_scene(config, seed, L, R, level_res, step, band_cells, ramp_cells, density_bias, source_mask,
+                mlp_scale, contraction):
     base = dict(CONFIGS["c1" if config == "c1" else "c2"])
     if L is not None:
         base["L"] = L
@@ -365,7 +408,8 @@ def make_scene(config: str = "c1", seed: int = SEED, L=None, R=None, level_res=N
         R = 0
     sc = MerfScene(L=L, R=R, level_res=level_res, step=step, planes=planes,
                    block_index=block_index, atlas=atlas, occ_finest=pack_bits(occ),
-                   mlp=_mlp_weights(seed, mlp_scale), source_mask=source_mask, name=config)
+                   mlp=_mlp_weights(seed, mlp_scale), source_mask=source_mask,
+                   name=config + ("_sph" if contraction == "sph" else ""))
     return sc
 
 

@@ -595,8 +595,20 @@ void orc_march(const orc_scene *S, const double o[3], const double d[3], double 
     if (trace_count) *trace_count = ntr;
 }
 
+void orc_march_sph(const orc_scene *S, const double o[3], const double d[3], double t_near,
+                   uint32_t flags, orc_ray_result *res, int32_t max_trace, uint64_t *trace_cells,
+                   double *trace_T, int32_t *trace_count);
+
+static void orc_march_any(const orc_scene *S, const double o[3], const double d[3], double t_near, int mode,
+                          uint32_t flags, orc_ray_result *res, int32_t max_trace, uint64_t *trace_cells,
+                          double *trace_T, int32_t *trace_count)
+{
+    if (mode == 2) orc_march_sph(S, o, d, t_near, flags, res, max_trace, trace_cells, trace_T, trace_count);
+    else orc_march(S, o, d, t_near, mode, flags, res, max_trace, trace_cells, trace_T, trace_count);
+}
+
 /* ---------------------------------------------------------------------------------- */
-/* Image / pixel-list renderers.  stats (optional, int64[6]): rays, segments, evals,  */
+/* Image / pixel-list renderers (mode 0 hierarchical, 1 dense, 2 spherical NEXT-2).  stats (optional, int64[6]): rays, segments, evals,  */
 /* density-only, skips, missing.                                                       */
 /* ---------------------------------------------------------------------------------- */
 void orc_render_pixels(const orc_scene *S, const double *cam, int32_t W, const int64_t *pixel_ids,
@@ -617,7 +629,7 @@ void orc_render_pixels(const orc_scene *S, const double *cam, int32_t W, const i
             double o[3], d[3];
             orc_raygen(cam, i, j, o, d);
             orc_ray_result res;
-            orc_march(S, o, d, cam[16], mode, flags, &res, max_trace,
+            orc_march_any(S, o, d, cam[16], mode, flags, &res, max_trace,
                       trace_cells ? trace_cells + r * max_trace : NULL,
                       trace_T ? trace_T + r * max_trace : NULL,
                       trace_count ? trace_count + r : NULL);
@@ -646,7 +658,7 @@ void orc_render_rays(const orc_scene *S, const double *o, const double *d, const
     int64_t st[6] = {0, 0, 0, 0, 0, 0};
     for (int64_t r = 0; r < n; r++) {
         orc_ray_result res;
-        orc_march(S, o + 3 * r, d + 3 * r, t_near ? t_near[r] : 0.0, mode, flags, &res, max_trace,
+        orc_march_any(S, o + 3 * r, d + 3 * r, t_near ? t_near[r] : 0.0, mode, flags, &res, max_trace,
                   trace_cells ? trace_cells + r * max_trace : NULL,
                   trace_T ? trace_T + r * max_trace : NULL,
                   trace_count ? trace_count + r : NULL);
@@ -732,4 +744,112 @@ void orc_pack_atlas(const uint8_t *dense, int32_t L, const int32_t *block_index,
                     for (int c = 0; c < 8; c++) dst[c] = src[c];
                 }
     }
+}
+
+/* ---------------------------------------------------------------------------------- */
+/* NEXT-2: the mip-NeRF 360 spherical contraction (Eq. 4) as a comparison   */
+/* variant.  It maps lines to curves, so there is no ray-AABB skip: samples */
+/* are taken at uniform contracted arc length (reading S1) by Euler steps               */
+/*   t_{k+1} = t_k + Delta / sigma(t_k),  sigma = |d/dt contract(o + t d)|,             */
+/* every sample is tested against the finest occupancy level, and the ray stops when    */
+/* the contracted radius reaches 2 - Delta.  Canonical fp64 order (D8) as written.      */
+/* ---------------------------------------------------------------------------------- */
+/* contract(x) of Eq. 4: x if |x| <= 1 else (2 - 1/|x|) x/|x|.  Returns |x|. */
+double orc_contract_sph(const double x[3], double c[3])
+{
+    double r2 = x[0] * x[0] + x[1] * x[1];
+    r2 = r2 + x[2] * x[2];
+    double r = sqrt(r2);
+    if (r <= 1.0) { c[0] = x[0]; c[1] = x[1]; c[2] = x[2]; return r; }
+    double s = 2.0 - 1.0 / r;
+    for (int k = 0; k < 3; k++) { double xh = x[k] / r; c[k] = s * xh; }
+    return r;
+}
+
+/* contracted speed sigma at x along unit d (derivative of Eq. 4 along the ray) */
+double orc_sph_speed(const double x[3], const double d[3])
+{
+    double r2 = x[0] * x[0] + x[1] * x[1];
+    r2 = r2 + x[2] * x[2];
+    double r = sqrt(r2);
+    if (r <= 1.0) return 1.0;
+    double xh[3];
+    for (int k = 0; k < 3; k++) xh[k] = x[k] / r;
+    double dr = d[0] * xh[0] + d[1] * xh[1];
+    dr = dr + d[2] * xh[2];
+    double rr = r * r;
+    double a = dr / rr;                          /* radial: d(2 - 1/r)/dr = 1/r^2       */
+    double b = (2.0 * r - 1.0) / rr;             /* tangential: (2 - 1/r)/r             */
+    double perp = 1.0 - dr * dr;
+    if (perp < 0.0) perp = 0.0;
+    double s2 = a * a + (b * b) * perp;
+    return sqrt(s2);
+}
+
+#define ORC_SPH_MAXK(step) ((int64_t)(8.0 / (step)) + 8)
+
+void orc_march_sph(const orc_scene *S, const double o[3], const double d[3], double t_near,
+                   uint32_t flags, orc_ray_result *res, int32_t max_trace, uint64_t *trace_cells,
+                   double *trace_T, int32_t *trace_count)
+{
+    double T = 1.0, cd[3] = {0, 0, 0}, F[4] = {0, 0, 0, 0};
+    int64_t n_eval = 0, n_donly = 0, n_missing = 0;
+    int32_t ntr = 0;
+    int nl = S->n_levels;
+    int32_t Nf = S->level_res[nl - 1];
+    double t = t_near;
+    const double stop = 2.0 - S->step;
+    const int64_t kmax = ORC_SPH_MAXK(S->step);
+    for (int64_t k = 0; k < kmax; k++) {
+        double x[3], c[3];
+        point_at(o, d, t, x);
+        double r = orc_contract_sph(x, c);
+        double cr = (r <= 1.0) ? r : (2.0 - 1.0 / r);
+        if (cr >= stop) break;
+        int64_t Q[3], cc[3];
+        for (int a = 0; a < 3; a++) {
+            Q[a] = llrint(c[a] * (double)ORC_ONE);
+            cc[a] = occ_cell(Q[a], Nf);
+        }
+        if (get_bit(S->occ[nl - 1], (cc[2] * Nf + cc[1]) * Nf + cc[0])) {
+            double tv[8];
+            n_missing += orc_query_field(S, Q, tv);
+            double tau = exp(tv[0]);
+            double alpha = 1.0 - exp(-(tau * S->step));
+            n_eval++;
+            if (alpha > S->alpha_skip) {
+                double w = alpha * T;
+                for (int q = 0; q < 3; q++) cd[q] += w * sigmoid(tv[1 + q]);
+                for (int q = 0; q < 4; q++) F[q] += w * sigmoid(tv[4 + q]);
+            } else {
+                n_donly++;
+            }
+            T = T * (1.0 - alpha);
+            if (trace_cells && ntr < max_trace) {
+                uint64_t cell = (uint64_t)((cc[2] * Nf + cc[1]) * Nf + cc[0]);
+                trace_cells[ntr] = ((uint64_t)k << 40) | cell;
+                trace_T[ntr] = T;
+            }
+            ntr++;
+            if (!(flags & ORC_NO_EARLY_TERM) && T < S->t_min) break;
+        }
+        double sig = orc_sph_speed(x, d);
+        t = t + S->step / sig;
+    }
+    double h[3];
+    orc_mlp(S->mlp, cd, F, d, h);
+    for (int q = 0; q < 3; q++) {
+        double v = cd[q] + h[q];
+        res->rgb[q] = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
+        res->cd[q] = cd[q];
+    }
+    for (int q = 0; q < 4; q++) res->F[q] = F[q];
+    res->T = T;
+    res->n_eval = n_eval;
+    res->n_density_only = n_donly;
+    res->n_skip = 0;
+    res->n_missing = n_missing;
+    res->n_seg = 1;
+    res->region_mask = 1;
+    if (trace_count) *trace_count = ntr;
 }

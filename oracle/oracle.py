@@ -84,6 +84,10 @@ def lib():
             L.orc_render_rays.argtypes = [vp, vp, vp, vp, i64, C.c_int, C.c_uint32, vp, vp,
                                           i32, vp, vp, vp, vp]
             L.orc_max_threads.restype = i32
+            L.orc_contract_sph.argtypes = [vp, vp]
+            L.orc_contract_sph.restype = dbl
+            L.orc_sph_speed.argtypes = [vp, vp]
+            L.orc_sph_speed.restype = dbl
             L.orc_bake_occupancy.argtypes = [vp, vp, vp, i64, dbl, dbl, i32, vp]
             L.orc_pack_atlas.argtypes = [vp, i32, vp, i64, vp]
             _lib = L
@@ -231,6 +235,7 @@ def mlp(w, cd, F, d):
 # ------------------------------------------------------------------------------------
 # renderers
 # ------------------------------------------------------------------------------------
+_MODES = {"hier": 0, "dense": 1, "sph": 2}
 STAT_KEYS = ("rays", "segments", "evaluated", "density_only", "skips", "missing")
 
 
@@ -254,7 +259,7 @@ def render(osc: OracleScene, cam, W: int, H: int, *, pixels=None, mode: str = "h
     rm = np.zeros(n, np.int32) if region_masks else None
     st = np.zeros(6, np.int64)
     nullp = C.c_void_p(0)
-    lib().orc_render_pixels(osc.ptr, _p(cam), int(W), _p(pixels), n, 0 if mode == "hier" else 1,
+    lib().orc_render_pixels(osc.ptr, _p(cam), int(W), _p(pixels), n, _MODES[mode],
                             int(flags), _p(rgb), _p(auxa) if aux else nullp, int(max_trace),
                             _p(tc) if max_trace else nullp, _p(tT) if max_trace else nullp,
                             _p(cnt) if max_trace else nullp, _p(st),
@@ -282,7 +287,7 @@ def render_rays(osc: OracleScene, o, d, t_near=None, *, mode: str = "hier", flag
     cnt = np.zeros(n, np.int32) if max_trace else None
     st = np.zeros(6, np.int64)
     nullp = C.c_void_p(0)
-    lib().orc_render_rays(osc.ptr, _p(o), _p(d), _p(tn), n, 0 if mode == "hier" else 1, int(flags),
+    lib().orc_render_rays(osc.ptr, _p(o), _p(d), _p(tn), n, _MODES[mode], int(flags),
                           _p(rgb), _p(auxa), int(max_trace), _p(tc) if max_trace else nullp,
                           _p(tT) if max_trace else nullp, _p(cnt) if max_trace else nullp, _p(st))
     out = dict(rgb=rgb, aux=auxa, stats=dict(zip(STAT_KEYS, st.tolist())))
@@ -328,3 +333,18 @@ def pack_atlas(dense, L: int, block_index, n_blocks: int):
     atlas = np.zeros((n_blocks, 9, 9, 9, 8), np.uint8)
     lib().orc_pack_atlas(_p(dense), int(L), _p(bi), int(n_blocks), _p(atlas))
     return atlas
+
+
+# ------------------------------------------------------------------------------------
+# NEXT-2: spherical contraction (Eq. 4)
+# ------------------------------------------------------------------------------------
+def contract_sph(x):
+    x = _c(x, np.float64).reshape(-1, 3)
+    y = np.empty_like(x)
+    for i in range(len(x)):
+        lib().orc_contract_sph(_p(x[i]), _p(y[i]))
+    return y
+
+
+def sph_speed(x, d) -> float:
+    return float(lib().orc_sph_speed(_p(_c(x, np.float64)), _p(_c(d, np.float64))))

@@ -400,6 +400,11 @@ static cudaError_t call_march(void* p) {
     ChunkCall* c = (ChunkCall*)p;
     return launch_march(c->kf_march, c->s->dev, c->rs->n, *c->ws, c->flags, *c->ta, c->d_stats, c->st);
 }
+static cudaError_t call_march_sph(void* p) {
+    ChunkCall* c = (ChunkCall*)p;
+    // the setup-variant flags carry RAYS/TRACE/COUNT for the single-kernel spherical path
+    return launch_march_sph(c->kf_setup, c->s->dev, *c->rs, *c->ws, c->flags, *c->ta, c->d_stats, c->st);
+}
 static cudaError_t call_shade(void* p) {
     ChunkCall* c = (ChunkCall*)p;
     return launch_shade(c->kf_shade, c->s->dev, *c->rs, *c->ws, c->out, c->st);
@@ -409,6 +414,12 @@ static merf_status run_chunk(const merf_scene* s, int kf_setup, int kf_march, in
                              const RaySource& rs, const Workspace& ws, void* out, uint32_t flags,
                              const TraceArgs& ta, unsigned long long* d_stats, cudaStream_t st) {
     ChunkCall c{s, kf_setup, kf_march, kf_shade, &rs, &ws, out, flags, &ta, d_stats, st};
+    if (flags & MERF_SPHERICAL) {          // NEXT-2 variant: no setup kernel, one march kernel
+        merf_status e = timed_launch(s, flags, 1, st, call_march_sph, &c);
+        if (e) return e;
+        if (kf_shade >= 0 && (e = timed_launch(s, flags, 2, st, call_shade, &c))) return e;
+        return MERF_OK;
+    }
     merf_status e = timed_launch(s, flags, 0, st, call_setup, &c);
     if (e) return e;
     if (kf_march >= 0 && (e = timed_launch(s, flags, 1, st, call_march, &c))) return e;

@@ -15,6 +15,8 @@ cudaError_t launch_setup(int kf, const DevScene& S, const RaySource& rs, const W
                          const TraceArgs& ta, unsigned long long* stats, cudaStream_t st);
 cudaError_t launch_march(int kf, const DevScene& S, int64_t n, const Workspace& ws, uint32_t rflags,
                          const TraceArgs& ta, unsigned long long* stats, cudaStream_t st);
+cudaError_t launch_march_sph(int kf, const DevScene& S, const RaySource& rs, const Workspace& ws,
+                             uint32_t rflags, const TraceArgs& ta, unsigned long long* stats, cudaStream_t st);
 cudaError_t launch_shade(int kf, const DevScene& S, const RaySource& rs, const Workspace& ws, void* out,
                          cudaStream_t st);
 

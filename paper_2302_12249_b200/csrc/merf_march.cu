@@ -53,4 +53,25 @@ cudaError_t launch_march(int kf, const DevScene& S, int64_t n, const Workspace& 
     }
 }
 
+template <int KF>
+static cudaError_t sph_v(const DevScene& S, const RaySource& rs, const Workspace& ws, uint32_t rflags,
+                         const TraceArgs& ta, unsigned long long* stats, cudaStream_t st) {
+    if (rs.n <= 0) return cudaSuccess;
+    dim3 grid((unsigned)((rs.n + kSetupThreads - 1) / kSetupThreads));
+    march_sph_kernel<KF><<<grid, kSetupThreads, 0, st>>>(S, rs, ws, rflags, ta, stats);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_march_sph(int kf, const DevScene& S, const RaySource& rs, const Workspace& ws,
+                             uint32_t rflags, const TraceArgs& ta, unsigned long long* stats, cudaStream_t st) {
+    switch (kf & (KF_TRACE | KF_RAYS | KF_COUNT)) {
+        case 0: return sph_v<0>(S, rs, ws, rflags, ta, stats, st);
+        case KF_COUNT: return sph_v<KF_COUNT>(S, rs, ws, rflags, ta, stats, st);
+        case KF_RAYS: return sph_v<KF_RAYS>(S, rs, ws, rflags, ta, stats, st);
+        case KF_RAYS | KF_COUNT: return sph_v<KF_RAYS | KF_COUNT>(S, rs, ws, rflags, ta, stats, st);
+        case KF_TRACE: return sph_v<KF_TRACE>(S, rs, ws, rflags, ta, stats, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
 }  // namespace merf

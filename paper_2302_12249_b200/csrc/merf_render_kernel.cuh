@@ -492,6 +492,120 @@ __global__ void __launch_bounds__(kMarchThreads, 4) march_kernel(DevScene S, int
 }
 
 // ====================================================================================
+// 2b. NEXT-2 comparison variant: the spherical contraction of Eq. 4.  Lines
+// map to curves, so there is no ray-AABB skip: one thread per ray takes Euler
+// steps of uniform contracted arc length, t += Delta / sigma(t) (reading S1), tests every
+// sample against the finest occupancy level and shades occupied samples with the same
+// gather/composite code.  Canonical fp64 stepping (reading D8: bit-reproducible traces).
+// ====================================================================================
+__device__ __forceinline__ double contract_sph(const double x[3], double c[3]) {
+    const double r = __dsqrt_rn(add_rn(add_rn(mul_rn(x[0], x[0]), mul_rn(x[1], x[1])), mul_rn(x[2], x[2])));
+    if (r <= 1.0) {
+        c[0] = x[0]; c[1] = x[1]; c[2] = x[2];
+        return r;
+    }
+    const double sc = sub_rn(2.0, div_rn(1.0, r));
+#pragma unroll
+    for (int q = 0; q < 3; q++) c[q] = mul_rn(sc, div_rn(x[q], r));
+    return r;
+}
+
+__device__ __forceinline__ double sph_speed(const double x[3], const double d[3], double r) {
+    if (r <= 1.0) return 1.0;
+    double xh[3];
+#pragma unroll
+    for (int q = 0; q < 3; q++) xh[q] = div_rn(x[q], r);
+    const double dr = add_rn(add_rn(mul_rn(d[0], xh[0]), mul_rn(d[1], xh[1])), mul_rn(d[2], xh[2]));
+    const double rr = mul_rn(r, r);
+    const double a = div_rn(dr, rr);
+    const double b = div_rn(sub_rn(mul_rn(2.0, r), 1.0), rr);
+    double perp = sub_rn(1.0, mul_rn(dr, dr));
+    if (perp < 0.0) perp = 0.0;
+    return __dsqrt_rn(add_rn(mul_rn(a, a), mul_rn(mul_rn(b, b), perp)));
+}
+
+template <int KF>
+__global__ void __launch_bounds__(kSetupThreads) march_sph_kernel(DevScene S, RaySource rs, Workspace ws,
+                                                                  uint32_t rflags, TraceArgs ta,
+                                                                  unsigned long long* stats) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t ray = rs.ray0 + r;
+    bool valid = r < rs.n;
+    double o[3] = {0, 0, 0}, d[3] = {0, 0, 1}, t = 0.0;
+    if (valid) {
+        if (KF & KF_TRACE) {
+            const int64_t pid = rs.pixel_ids[ray];
+            raygen(rs.cb.cam[0], (int)(pid % rs.W), (int)(pid / rs.W), o, d);
+            t = rs.cb.cam[0].t_near;
+        } else if (KF & KF_RAYS) {
+#pragma unroll
+            for (int q = 0; q < 3; q++) { o[q] = rs.o[3 * ray + q]; d[q] = rs.d[3 * ray + q]; }
+            t = rs.t_near ? rs.t_near[ray] : 0.0;
+        } else {
+            int view, px, py;
+            valid = ray_pixel(rs, ray, view, px, py);
+            if (valid) {
+                raygen(rs.cb.cam[view], px, py, o, d);
+                t = rs.cb.cam[view].t_near;
+            }
+        }
+    }
+    RayState st;
+    st.T = 1.f;
+    st.cd[0] = st.cd[1] = st.cd[2] = 0.f;
+    st.F[0] = st.F[1] = st.F[2] = st.F[3] = 0.f;
+    int n_eval = 0, c_donly = 0, c_miss = 0;
+    int bslot = -1, bblk = -1;
+    if (valid) {
+        const int nl = S.n_levels;
+        const int Nf = S.level_res[nl - 1];
+        const int sf = S.level_shift[nl - 1];
+        const double stop = sub_rn(2.0, S.step);
+        const int kmax = (int)(8.0 / S.step) + 8;
+        for (int k = 0; k < kmax; k++) {
+            double x[3], c[3];
+            point_at(o, d, t, x);
+            const double rad = contract_sph(x, c);
+            const double cr = rad <= 1.0 ? rad : sub_rn(2.0, div_rn(1.0, rad));
+            if (cr >= stop) break;
+            const int Qx = (int)__double2ll_rn(mul_rn(c[0], (double)kOne));
+            const int Qy = (int)__double2ll_rn(mul_rn(c[1], (double)kOne));
+            const int Qz = (int)__double2ll_rn(mul_rn(c[2], (double)kOne));
+            const int fx = occ_cell(Qx, sf, Nf), fy = occ_cell(Qy, sf, Nf), fz = occ_cell(Qz, sf, Nf);
+            if (occ_bit(S.occ[nl - 1], fx, fy, fz, Nf)) {
+                const int kind = shade_sample<KF>(S, Qx, Qy, Qz, st, bslot, bblk);
+                c_donly += kind == 1;
+                c_miss += kind == 2;
+                if (KF & KF_TRACE) {
+                    if (n_eval < ta.max_per_ray) {
+                        const int64_t idx = ray * ta.max_per_ray + n_eval;
+                        ta.cells[idx] = ((uint64_t)k << 40) | (uint64_t)((fz * Nf + fy) * Nf + fx);
+                        if (ta.T) ta.T[idx] = st.T;
+                    }
+                }
+                n_eval++;
+                if (!(rflags & MERF_NO_EARLY_TERM) && st.T < S.t_min) break;
+            }
+            t = add_rn(t, div_rn(S.step, sph_speed(x, d, rad)));
+        }
+    }
+    if (r < rs.n) {
+        float4* a = ws.accum + r * 2;
+        a[0] = make_float4(st.cd[0], st.cd[1], st.cd[2], st.T);
+        a[1] = make_float4(st.F[0], st.F[1], st.F[2], st.F[3]);
+        if (KF & KF_TRACE) ta.counts[ray] = n_eval;
+    }
+    if (KF & KF_COUNT) {
+        add_stat(stats, 0, valid ? 1 : 0);
+        add_stat(stats, 1, valid ? 1 : 0);
+        add_stat(stats, 2, n_eval);
+        add_stat(stats, 3, c_donly);
+        add_stat(stats, 5, c_miss);
+        add_stat(stats, 6, valid ? 1 : 0);
+    }
+}
+
+// ====================================================================================
 // 3. deferred MLP + store
 // ====================================================================================
 __device__ __forceinline__ void deferred_mlp(const float* __restrict__ w, const float x7[7],
