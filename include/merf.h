@@ -286,6 +286,49 @@ merf_status merf_bake_occupancy(const double *x, const double *tau, const double
 merf_status merf_pack_atlas(const uint8_t *dense, int32_t L, const int32_t *index, int64_t n_blocks,
                             uint8_t *atlas_out, void *stream);
 
+/*
+ * Quantisation-aware training step (Sec. 5.2, Eq. 7-8) on
+ * toy DENSE grids: continuous pre-sigmoid parameters theta of a dense L^3 grid and three R^2
+ * planes (C = 8 channels, channel fastest, same axis conventions as the baked arrays) are
+ * turned into stored values v = 2m q(sigma(theta)) - m (Eq. 7; q = round to 1/255 when
+ * `quantize`, else identity), rendered with the renderer's lattice (readings D5-D8) at every
+ * sample inside an occupied cell of `occ` (dense mode, no early termination), composited
+ * (Eq. 1-2) and shaded by the fixed deferred MLP (Eq. 3) into C = clamp(C_d + h, 0, 1).
+ * Texel lookup clamps the lower corner to [0, M-2] (same values as reading D9's clamp, and
+ * gradients never leave the grid).  loss = sum over pixels and channels (C - target)^2; the
+ * gradient of the loss w.r.t. theta uses the straight-through estimator dq/dx = 1 (Eq. 8).
+ */
+typedef struct {
+    int32_t L;                  /* dense grid resolution (power of two, 2..1024)              */
+    int32_t R;                  /* plane resolution (power of two, 2..8192)                   */
+    int32_t occ_res;            /* occupancy grid resolution N (power of two, 2..4096)        */
+    int32_t quantize;           /* 1: Eq. 7-8 with STE; 0: continuous sigma(theta)            */
+    int32_t max_samples;        /* per-ray sample records kept for the backward pass (>= 1)   */
+    int32_t pad_;
+    double step;                /* Delta (power of two in (0, 1])                             */
+    double m_density, m_appearance;   /* decode ranges m: 14 and 7                     */
+} merf_qat_desc;
+
+/*
+ * merf_qat_step: forward + backward of one batch of n_cams views (<= 16).
+ *   theta_v [device] float [L][L][L][8]; theta_p [device] float [3][R][R][8];
+ *   occ [device] uint32 bits of the N^3 occupancy grid (x fastest, LSB first);
+ *   mlp [device] float [883]; cams [host] merf_camera [n_cams];
+ *   target [device] float [n_cams][H][W][3];
+ *   rgb_out [device] float [n_cams][H][W][3] (written);
+ *   grad_v, grad_p [device] float, shaped like theta (overwritten, not accumulated);
+ *   loss [device] double (overwritten);
+ *   overflow [device] int32 or NULL: rays whose sample count exceeded max_samples (their
+ *   colour and loss are exact, their gradient contribution is dropped; 0 on a valid call).
+ * Scratch (~48 B x max_samples per ray) is stream-ordered device memory owned by the call.
+ * Asynchronous on `stream`.  Errors: MERF_EINVAL (null pointers, bad sizes), MERF_ENOMEM,
+ * MERF_ECUDA.
+ */
+merf_status merf_qat_step(const merf_qat_desc *desc, const float *theta_v, const float *theta_p,
+                          const uint32_t *occ, const float *mlp, const merf_camera *cams,
+                          int32_t n_cams, int32_t W, int32_t H, const float *target, float *rgb_out,
+                          float *grad_v, float *grad_p, double *loss, int32_t *overflow, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

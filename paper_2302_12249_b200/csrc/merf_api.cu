@@ -721,3 +721,68 @@ extern "C" merf_status merf_pack_atlas(const uint8_t* dense, int32_t L, const in
     CUDA_TRY(launch_pack_atlas(dense, L, index, n_blocks, atlas_out, (cudaStream_t)stream));
     return MERF_OK;
 }
+
+// ------------------------------------------------------------------------------------
+// NEXT-3: quantisation-aware training step on toy dense grids (Eq. 7-8)
+// ------------------------------------------------------------------------------------
+extern "C" merf_status merf_qat_step(const merf_qat_desc* d, const float* theta_v, const float* theta_p,
+                                     const uint32_t* occ, const float* mlp, const merf_camera* cams,
+                                     int32_t n_cams, int32_t W, int32_t H, const float* target, float* rgb_out,
+                                     float* grad_v, float* grad_p, double* loss, int32_t* overflow,
+                                     void* stream) {
+    if (!d || !theta_v || !theta_p || !occ || !mlp || !cams || !target || !rgb_out || !grad_v || !grad_p || !loss)
+        return fail(MERF_EINVAL, "NULL argument");
+    if (!is_pow2(d->L) || d->L < 2 || d->L > 1024 || !is_pow2(d->R) || d->R < 2 || d->R > 8192)
+        return fail(MERF_EINVAL, "L, R must be powers of two in [2, 1024] / [2, 8192]");
+    if (!is_pow2(d->occ_res) || d->occ_res < 2 || d->occ_res > 4096)
+        return fail(MERF_EINVAL, "occ_res must be a power of two in [2, 4096]");
+    if (d->max_samples < 1 || d->max_samples > (1 << 20)) return fail(MERF_EINVAL, "bad max_samples");
+    int ex = 0;
+    if (!(d->step > 0.0 && d->step <= 1.0) || std::frexp(d->step, &ex) != 0.5)
+        return fail(MERF_EINVAL, "step must be a power of two in (0, 1]");
+    if (!(d->m_density > 0.0) || !(d->m_appearance > 0.0)) return fail(MERF_EINVAL, "bad decode range m");
+    if (n_cams <= 0 || n_cams > kMaxCams || W <= 0 || H <= 0) return fail(MERF_EINVAL, "bad n_cams, W or H");
+    RaySource rs{};
+    rs.W = W;
+    rs.H = H;
+    rs.tiles_x = (W + 7) / 8;
+    rs.tiles_per_view = rs.tiles_x * ((H + 3) / 4);
+    rs.n = (int64_t)rs.tiles_per_view * 32 * n_cams;
+    if (rs.n * d->max_samples > (int64_t(1) << 31)) return fail(MERF_EINVAL, "n_rays * max_samples > 2^31");
+    rs.cb.n = n_cams;
+    for (int i = 0; i < n_cams; i++) rs.cb.cam[i] = cams[i];
+    DevScene S{};
+    S.step = d->step;
+    S.lattice_step = std::ldexp(d->step, kF);
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t nv = (int64_t)d->L * d->L * d->L * 8, np = (int64_t)3 * d->R * d->R * 8;
+    const size_t samp_b = align256((size_t)rs.n * d->max_samples * 48);
+    const size_t grid_b = align256((size_t)(nv + np) * 4);
+    void* base = nullptr;
+    Workspace ws;
+    merf_status e = ws_alloc(rs.n, st, ws, &base);
+    if (e) return e;
+    char* scratch = nullptr;
+    if (cudaMallocAsync((void**)&scratch, samp_b + 2 * grid_b + 256, st) != cudaSuccess) {
+        cudaFreeAsync(base, st);
+        return fail(MERF_ENOMEM, "QAT scratch allocation failed");
+    }
+    float* samp = (float*)scratch;
+    float* vv = (float*)(scratch + samp_b);
+    float* vp = vv + nv;
+    float* gvv = (float*)(scratch + samp_b + grid_b);
+    float* gvp = gvv + nv;
+    unsigned int* ovf = overflow ? (unsigned int*)overflow : (unsigned int*)(scratch + samp_b + 2 * grid_b);
+    cudaError_t ce = cudaMemsetAsync(ovf, 0, 4, st);
+    if (ce == cudaSuccess) ce = cudaMemsetAsync(loss, 0, 8, st);
+    TraceArgs ta{};
+    if (ce == cudaSuccess) ce = launch_setup(0, S, rs, ws, ta, nullptr, st);
+    if (ce == cudaSuccess)
+        ce = launch_qat(S, rs, ws, theta_v, theta_p, vv, vp, d->quantize ? 1 : 0, target, rgb_out, gvv, gvp,
+                        grad_v, grad_p, samp, d->max_samples, mlp, loss, ovf, d->L, d->R, d->occ_res, occ,
+                        (float)d->m_density, (float)d->m_appearance, st);
+    cudaFreeAsync(scratch, st);
+    cudaFreeAsync(base, st);
+    if (ce != cudaSuccess) return fail(MERF_ECUDA, "%s", cudaGetErrorString(ce));
+    return MERF_OK;
+}

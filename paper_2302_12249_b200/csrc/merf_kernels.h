@@ -40,4 +40,14 @@ cudaError_t launch_pack_atlas(const uint8_t* dense, int L, const int32_t* index,
                               uint8_t* atlas, cudaStream_t st);
 cudaError_t launch_contract(const double* x, int64_t n, double* y, int32_t* region, cudaStream_t st);
 
+// NEXT-3 quantisation-aware forward/backward (merf_qat.cu)
+struct DevScene;
+struct RaySource;
+struct Workspace;
+cudaError_t launch_qat(const DevScene& S, const RaySource& rs, const Workspace& ws, const float* theta_v,
+                       const float* theta_p, float* vv, float* vp, int quant, const float* target, float* rgb,
+                       float* gvals_v, float* gvals_p, float* grad_v, float* grad_p, float* samp, int smax,
+                       const float* mlp, double* loss, unsigned int* overflow, int L, int R, int Nf,
+                       const uint32_t* occf, float md, float ma, cudaStream_t st);
+
 }  // namespace merf

@@ -1,0 +1,269 @@
+// merf_qat.cu -- NEXT-3: quantisation-aware differentiable forward/backward of the render path
+// on toy dense grids (Sec. 5.2, Eq. 7-8).
+//
+//  1. prequant_kernel: stored value v = 2m q(sigma(theta)) - m per grid element (Eq. 7), with
+//     q(x) = floor(255 x + 1/2)/255 (Eq. 8) evaluated in fp64 so byte decisions are exact.
+//  2. qat_ray_kernel (one thread per ray; lattice from the render setup kernel, every sample
+//     in an occupied finest cell, no early termination): forward gather (Eq. 5), decode
+//     (Eq. 6), composite (Eq. 1-2) storing per-sample records; deferred MLP (Eq. 3) forward
+//     and backward; loss sum (C - C*)^2; then the reverse compositing pass
+//        dL/dalpha_i = T_i (G . x_i - G . R_i),  R_i = sum_{j>i} alpha_j prod_{i<k<j}(1-alpha_k) x_j
+//     (division-free), chained to dL/dt and scattered to the grid corners with atomics.
+//  3. ste_kernel: dL/dtheta = dL/dv * 2m sigma'(theta) -- the straight-through estimator
+//     treats q as the identity in the backward pass (Eq. 8).
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "merf_render_kernel.cuh"
+
+namespace merf {
+
+struct QatArgs {
+    const float* vv;        // [L^3][8] stored (quantised) values of V
+    const float* vp;        // [3][R^2][8] stored values of the planes
+    const float* target;    // [H*W][3]
+    float* rgb;             // [H*W][3]
+    float* gv;              // [L^3][8] dL/dv (accumulated)
+    float* gp;              // [3][R^2][8]
+    float* samp;            // [n][smax][12]
+    const float* mlp;       // [883]
+    double* loss;
+    unsigned int* overflow;
+    int L, R, smax, Nf, sf;
+    const uint32_t* occf;
+    float step;
+};
+
+__device__ __forceinline__ void coord_qat(int Q, int M, int& i0, float& f) {
+    // lower texel index in [0, M-2] and fraction (cell-centred, clamp to edge; reading D9)
+    const int s = kF + 2 - (31 - __clz(M));
+    const int P = Q + kTwoI - (1 << (s - 1));
+    int i = P >> s;
+    float fr = (float)(P & ((1 << s) - 1)) * __int_as_float((127 - s) << 23);
+    if (i < 0) { i = 0; fr = 0.f; }
+    if (i > M - 2) { i = M - 2; fr = 1.f; }
+    i0 = i;
+    f = fr;
+}
+
+// visit the 8 + 12 corners of lattice point Q: fn(grid (0 = V, 1..3 = plane), element, weight)
+template <typename Fn>
+__device__ __forceinline__ void for_corners(const QatArgs& A, int Qx, int Qy, int Qz, Fn fn) {
+    const int Q[3] = {Qx, Qy, Qz};
+    int vi[3];
+    float vf[3];
+#pragma unroll
+    for (int a = 0; a < 3; a++) coord_qat(Q[a], A.L, vi[a], vf[a]);
+#pragma unroll
+    for (int c = 0; c < 8; c++) {
+        const int dx = c & 1, dy = (c >> 1) & 1, dz = c >> 2;
+        const float w = (dx ? vf[0] : 1.f - vf[0]) * (dy ? vf[1] : 1.f - vf[1]) * (dz ? vf[2] : 1.f - vf[2]);
+        fn(0, ((vi[2] + dz) * A.L + (vi[1] + dy)) * A.L + (vi[0] + dx), w);
+    }
+    int pi[3];
+    float pf[3];
+#pragma unroll
+    for (int a = 0; a < 3; a++) coord_qat(Q[a], A.R, pi[a], pf[a]);
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+        const int ua = (a == 0) ? 1 : 0, va = (a == 2) ? 1 : 2;
+#pragma unroll
+        for (int c = 0; c < 4; c++) {
+            const int du = c & 1, dv = c >> 1;
+            const float w = (du ? pf[ua] : 1.f - pf[ua]) * (dv ? pf[va] : 1.f - pf[va]);
+            fn(1 + a, (pi[va] + dv) * A.R + (pi[ua] + du), w);
+        }
+    }
+}
+
+__global__ void prequant_kernel(const float* __restrict__ theta, int64_t n, int quant, float md, float ma,
+                                float* __restrict__ v) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double m = (i % 8 == 0) ? (double)md : (double)ma;
+    const double s = 1.0 / (1.0 + exp(-(double)theta[i]));
+    const double q = quant ? floor(255.0 * s + 0.5) / 255.0 : s;
+    v[i] = (float)(2.0 * m * q - m);
+}
+
+__global__ void ste_kernel(const float* __restrict__ theta, const float* __restrict__ gvals, int64_t n,
+                           float md, float ma, float* __restrict__ gtheta) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float m = (i % 8 == 0) ? md : ma;
+    const float s = 1.f / (1.f + expf(-theta[i]));
+    gtheta[i] = gvals[i] * 2.f * m * s * (1.f - s);
+}
+
+__global__ void __launch_bounds__(128) qat_ray_kernel(DevScene S, RaySource rs, Workspace ws, QatArgs A) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= rs.n) return;
+    int view, px, py;
+    if (!ray_pixel(rs, r, view, px, py)) return;
+    const int64_t pix = (int64_t)py * rs.W + px;
+    float* rec0 = A.samp + (size_t)r * A.smax * 12;
+    // ---------------- forward ----------------
+    float acc[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    float T = 1.f;
+    int n = 0;
+    bool over = false;
+    const int ns = ws.nseg[r];
+    for (int j = 0; j < ns; j++) {
+        const int4 qa = ws.seg[(r * kMaxSeg + j) * 2], uu = ws.seg[(r * kMaxSeg + j) * 2 + 1];
+        for (int k = 0; k < qa.w; k++) {
+            const int Qx = qa.x + k * uu.x, Qy = qa.y + k * uu.y, Qz = qa.z + k * uu.z;
+            if (!occ_bit(A.occf, occ_cell(Qx, A.sf, A.Nf), occ_cell(Qy, A.sf, A.Nf), occ_cell(Qz, A.sf, A.Nf), A.Nf))
+                continue;
+            float t[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            for_corners(A, Qx, Qy, Qz, [&](int g, int e, float w) {
+                const float* src = (g == 0) ? A.vv + (size_t)e * 8 : A.vp + ((size_t)(g - 1) * A.R * A.R + e) * 8;
+#pragma unroll
+                for (int c = 0; c < 8; c++) t[c] = fmaf(w, src[c], t[c]);
+            });
+            const float tau = expf(t[0]);
+            const float alpha = 1.f - expf(-tau * A.step);
+            if (n < A.smax) {
+                float* rec = rec0 + (size_t)n * 12;
+                rec[0] = __int_as_float(Qx);
+                rec[1] = __int_as_float(Qy);
+                rec[2] = __int_as_float(Qz);
+                rec[3] = t[0];
+                rec[4] = T;
+#pragma unroll
+                for (int c = 0; c < 7; c++) {
+                    const float x = 1.f / (1.f + expf(-t[1 + c]));
+                    rec[5 + c] = x;
+                    acc[c] = fmaf(alpha * T, x, acc[c]);
+                }
+            } else {
+                over = true;
+            }
+            T *= (1.f - alpha);
+            n++;
+        }
+    }
+    if (over) atomicAdd(A.overflow, 1u);
+    // ---------------- deferred MLP forward (Eq. 3) ----------------
+    double od[3], dd[3];
+    raygen(rs.cb.cam[view], px, py, od, dd);
+    float x[34];
+#pragma unroll
+    for (int c = 0; c < 7; c++) x[c] = acc[c];
+#pragma unroll
+    for (int q = 0; q < 3; q++) x[7 + q] = (float)dd[q];
+    int m = 10;
+#pragma unroll
+    for (int jj = 0; jj < 3; jj++)
+#pragma unroll
+        for (int kk = 0; kk < 4; kk++) {
+            const float a = (float)dd[jj] * (float)(1 << kk);
+            x[m++] = sinf(a);
+            x[m++] = cosf(a);
+        }
+    const float* W0 = A.mlp;
+    const float* b0 = A.mlp + 544;
+    const float* W1 = A.mlp + 560;
+    const float* b1 = A.mlp + 816;
+    const float* W2 = A.mlp + 832;
+    const float* b2 = A.mlp + 880;
+    float h0[16], h1[16], h[3];
+    for (int o = 0; o < 16; o++) {
+        float s = b0[o];
+        for (int i = 0; i < 34; i++) s = fmaf(W0[o * 34 + i], x[i], s);
+        h0[o] = fmaxf(s, 0.f);
+    }
+    for (int o = 0; o < 16; o++) {
+        float s = b1[o];
+        for (int i = 0; i < 16; i++) s = fmaf(W1[o * 16 + i], h0[i], s);
+        h1[o] = fmaxf(s, 0.f);
+    }
+    for (int o = 0; o < 3; o++) {
+        float s = b2[o];
+        for (int i = 0; i < 16; i++) s = fmaf(W2[o * 16 + i], h1[i], s);
+        h[o] = 1.f / (1.f + expf(-s));
+    }
+    float dC[3];
+    double lsum = 0.0;
+#pragma unroll
+    for (int c = 0; c < 3; c++) {
+        const float raw = acc[c] + h[c];
+        const float C = fminf(fmaxf(raw, 0.f), 1.f);
+        A.rgb[pix * 3 + c] = C;
+        const float e = C - A.target[pix * 3 + c];
+        lsum += (double)e * e;
+        dC[c] = (raw > 0.f && raw < 1.f) ? 2.f * e : 0.f;
+    }
+    atomicAdd(A.loss, lsum);
+    // ---------------- MLP backward -> G = dL/d(C_d, F) ----------------
+    float dz2[3], dh1[16], dh0[16];
+#pragma unroll
+    for (int o = 0; o < 3; o++) dz2[o] = dC[o] * h[o] * (1.f - h[o]);
+    for (int i = 0; i < 16; i++) {
+        float s = 0.f;
+        for (int o = 0; o < 3; o++) s = fmaf(W2[o * 16 + i], dz2[o], s);
+        dh1[i] = h1[i] > 0.f ? s : 0.f;
+    }
+    for (int i = 0; i < 16; i++) {
+        float s = 0.f;
+        for (int o = 0; o < 16; o++) s = fmaf(W1[o * 16 + i], dh1[o], s);
+        dh0[i] = h0[i] > 0.f ? s : 0.f;
+    }
+    float G[7];
+    for (int i = 0; i < 7; i++) {
+        float s = (i < 3) ? dC[i] : 0.f;
+        for (int o = 0; o < 16; o++) s = fmaf(W0[o * 34 + i], dh0[o], s);
+        G[i] = s;
+    }
+    if (over) return;
+    // ---------------- reverse compositing pass + scatter ----------------
+    float Rt[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int i = n - 1; i >= 0; i--) {
+        const float* rec = rec0 + (size_t)i * 12;
+        const float tau = expf(rec[3]);
+        const float alpha = 1.f - expf(-tau * A.step);
+        const float Ti = rec[4];
+        float gx = 0.f, gr = 0.f;
+#pragma unroll
+        for (int c = 0; c < 7; c++) {
+            gx = fmaf(G[c], rec[5 + c], gx);
+            gr = fmaf(G[c], Rt[c], gr);
+        }
+        const float dalpha = Ti * (gx - gr);
+#pragma unroll
+        for (int c = 0; c < 7; c++) Rt[c] = fmaf(alpha, rec[5 + c] - Rt[c], Rt[c]);   // a x + (1-a) R
+        float dt[8];
+        dt[0] = dalpha * A.step * (1.f - alpha) * tau;
+        const float w = alpha * Ti;
+#pragma unroll
+        for (int c = 0; c < 7; c++) dt[1 + c] = w * G[c] * rec[5 + c] * (1.f - rec[5 + c]);
+        for_corners(A, __float_as_int(rec[0]), __float_as_int(rec[1]), __float_as_int(rec[2]),
+                    [&](int g, int e, float wc) {
+                        float* dst = (g == 0) ? A.gv + (size_t)e * 8 : A.gp + ((size_t)(g - 1) * A.R * A.R + e) * 8;
+#pragma unroll
+                        for (int c = 0; c < 8; c++)
+                            if (wc != 0.f) atomicAdd(dst + c, wc * dt[c]);
+                    });
+    }
+}
+
+static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+cudaError_t launch_qat(const DevScene& S, const RaySource& rs, const Workspace& ws, const float* theta_v,
+                       const float* theta_p, float* vv, float* vp, int quant, const float* target, float* rgb,
+                       float* gvals_v, float* gvals_p, float* grad_v, float* grad_p, float* samp, int smax,
+                       const float* mlp, double* loss, unsigned int* overflow, int L, int R, int Nf,
+                       const uint32_t* occf, float md, float ma, cudaStream_t st) {
+    const int64_t nv = (int64_t)L * L * L * 8, np = (int64_t)3 * R * R * 8;
+    prequant_kernel<<<nblk(nv, 256), 256, 0, st>>>(theta_v, nv, quant, md, ma, vv);
+    prequant_kernel<<<nblk(np, 256), 256, 0, st>>>(theta_p, np, quant, md, ma, vp);
+    cudaMemsetAsync(gvals_v, 0, nv * 4, st);
+    cudaMemsetAsync(gvals_p, 0, np * 4, st);
+    QatArgs A{vv, vp, target, rgb, gvals_v, gvals_p, samp, mlp, loss, overflow, L, R, smax, Nf,
+              kF + 2 - (31 - __builtin_clz((unsigned)Nf)), occf, (float)S.step};
+    qat_ray_kernel<<<nblk(rs.n, 128), 128, 0, st>>>(S, rs, ws, A);
+    ste_kernel<<<nblk(nv, 256), 256, 0, st>>>(theta_v, gvals_v, nv, md, ma, grad_v);
+    ste_kernel<<<nblk(np, 256), 256, 0, st>>>(theta_p, gvals_p, np, md, ma, grad_p);
+    return cudaGetLastError();
+}
+
+}  // namespace merf

@@ -38,6 +38,12 @@ class merf_scene_desc(C.Structure):
                 ("source_mask", C.c_uint32)]
 
 
+class merf_qat_desc(C.Structure):
+    _fields_ = [("L", C.c_int32), ("R", C.c_int32), ("occ_res", C.c_int32), ("quantize", C.c_int32),
+                ("max_samples", C.c_int32), ("pad_", C.c_int32), ("step", C.c_double),
+                ("m_density", C.c_double), ("m_appearance", C.c_double)]
+
+
 class merf_camera(C.Structure):
     _fields_ = [("c2w", C.c_double * 12), ("fx", C.c_double), ("fy", C.c_double),
                 ("cx", C.c_double), ("cy", C.c_double), ("t_near", C.c_double)]
@@ -91,6 +97,8 @@ SIGNATURES = [
     ("merf_build_occupancy", C.c_int, [_vp, C.POINTER(merf_scene_desc), _vp, _vp]),
     ("merf_bake_occupancy", C.c_int, [_vp, _vp, _vp, _i64, _i32, C.c_double, C.c_double, C.c_double, _vp, _vp]),
     ("merf_pack_atlas", C.c_int, [_vp, _i32, _vp, _i64, _vp, _vp]),
+    ("merf_qat_step", C.c_int, [C.POINTER(merf_qat_desc), _vp, _vp, _vp, _vp, C.POINTER(merf_camera), _i32,
+                                _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     ("merf_build_block_index", C.c_int, [_vp, C.POINTER(merf_scene_desc), _vp, C.POINTER(_i64), _vp]),
 ]
 
@@ -281,6 +289,22 @@ def merf_bake_occupancy(x, tau, w, N: int, step: float, bits_out, w_thr: float =
 def merf_pack_atlas(dense, L: int, index, n_blocks: int, atlas_out, stream=None) -> None:
     _check(lib().merf_pack_atlas(_ptr(dense), int(L), _ptr(index), int(n_blocks), _ptr(atlas_out),
                                  _stream(stream)))
+
+
+def merf_qat_step(theta_v, theta_p, occ, N: int, mlp, cams, W: int, H: int, target, rgb_out, grad_v,
+                  grad_p, loss, step: float, quantize: bool = True, max_samples: int = 1024,
+                  overflow=None, m_density: float = 14.0, m_appearance: float = 7.0, stream=None) -> None:
+    """NEXT-3 quantisation-aware forward + backward (Eq. 7-8) on dense grids; every tensor is a
+    device tensor: theta_v [L,L,L,8] / theta_p [3,R,R,8] float32, occ uint32 bits of N^3,
+    target / rgb_out [n,H,W,3] float32, grad_* like theta, loss float64 [1], overflow int32 [1]."""
+    d = merf_qat_desc()
+    d.L, d.R, d.occ_res = int(theta_v.shape[0]), int(theta_p.shape[1]), int(N)
+    d.quantize, d.max_samples, d.step = int(bool(quantize)), int(max_samples), float(step)
+    d.m_density, d.m_appearance = float(m_density), float(m_appearance)
+    carr = cameras_to_c(cams)
+    _check(lib().merf_qat_step(C.byref(d), _ptr(theta_v), _ptr(theta_p), _ptr(occ), _ptr(mlp), carr, len(carr),
+                               int(W), int(H), _ptr(target), _ptr(rgb_out), _ptr(grad_v), _ptr(grad_p),
+                               _ptr(loss), _ptr(overflow), _stream(stream)))
 
 
 class Scene:

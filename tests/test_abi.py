@@ -45,9 +45,10 @@ def test_struct_layouts_match_c(M):
 #include <stddef.h>
 #include "merf.h"
 int main(void) {
-  printf("%zu %zu %zu %zu %zu %zu %zu\n", sizeof(merf_scene_desc), sizeof(merf_camera),
+  printf("%zu %zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(merf_scene_desc), sizeof(merf_camera),
          sizeof(merf_stats), sizeof(merf_scene_info), offsetof(merf_scene_desc, step),
-         offsetof(merf_scene_desc, source_mask), offsetof(merf_scene_info, n_blocks));
+         offsetof(merf_scene_desc, source_mask), offsetof(merf_scene_info, n_blocks),
+         sizeof(merf_qat_desc), offsetof(merf_qat_desc, step));
   return 0;
 }'''
     with tempfile.TemporaryDirectory() as d:
@@ -60,7 +61,8 @@ int main(void) {
     mm = M.merf
     expect = [C.sizeof(mm.merf_scene_desc), C.sizeof(mm.merf_camera), C.sizeof(mm.merf_stats),
               C.sizeof(mm.merf_scene_info), mm.merf_scene_desc.step.offset,
-              mm.merf_scene_desc.source_mask.offset, mm.merf_scene_info.n_blocks.offset]
+              mm.merf_scene_desc.source_mask.offset, mm.merf_scene_info.n_blocks.offset,
+              C.sizeof(mm.merf_qat_desc), mm.merf_qat_desc.step.offset]
     assert got == expect
 
 
