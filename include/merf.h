@@ -319,7 +319,8 @@ typedef struct {
  *   grad_v, grad_p [device] float, shaped like theta (overwritten, not accumulated);
  *   loss [device] double (overwritten);
  *   overflow [device] int32 or NULL: rays whose sample count exceeded max_samples (their
- *   colour and loss are exact, their gradient contribution is dropped; 0 on a valid call).
+ *   colour and loss are exact, their gradient contribution is dropped; 0 on a valid call);
+ *   n_samples [device] int64 or NULL: total evaluated samples of the batch.
  * Scratch (~48 B x max_samples per ray) is stream-ordered device memory owned by the call.
  * Asynchronous on `stream`.  Errors: MERF_EINVAL (null pointers, bad sizes), MERF_ENOMEM,
  * MERF_ECUDA.
@@ -327,7 +328,8 @@ typedef struct {
 merf_status merf_qat_step(const merf_qat_desc *desc, const float *theta_v, const float *theta_p,
                           const uint32_t *occ, const float *mlp, const merf_camera *cams,
                           int32_t n_cams, int32_t W, int32_t H, const float *target, float *rgb_out,
-                          float *grad_v, float *grad_p, double *loss, int32_t *overflow, void *stream);
+                          float *grad_v, float *grad_p, double *loss, int32_t *overflow, int64_t *n_samples,
+                          void *stream);
 
 #ifdef __cplusplus
 }

@@ -66,6 +66,16 @@ static int64_t occ_words(int N) { return ((int64_t)N * N * N + 31) / 32; }
 extern "C" const char* merf_last_error(void) { return g_err.c_str(); }
 extern "C" int32_t merf_version(void) { return 100; }
 
+// keep call workspaces cached in the device's stream-ordered pool between calls (no
+// re-mapping of pages per call)
+static void keep_pool_cached(int device) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+}
+
 static merf_status validate_desc(const merf_scene_desc* d) {
     if (!d) return fail(MERF_EINVAL, "desc is NULL");
     if (d->C != 8) return fail(MERF_EINVAL, "C must be 8 (got %d)", d->C);
@@ -185,13 +195,7 @@ extern "C" merf_status merf_scene_upload(const merf_scene_desc* desc, const uint
     // kernel on another stream could read stale device memory.
     cudaStream_t cs;
     UPC_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-    {   // keep render workspaces cached in the stream-ordered pool between calls
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-            uint64_t thr = UINT64_MAX;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-        }
-    }
+    keep_pool_cached(device);
     // ---- MLP weights
     float* d_mlp;
     UP_TRY(dalloc(s, &d_mlp, kMlpFloats * sizeof(float)));
@@ -729,7 +733,7 @@ extern "C" merf_status merf_qat_step(const merf_qat_desc* d, const float* theta_
                                      const uint32_t* occ, const float* mlp, const merf_camera* cams,
                                      int32_t n_cams, int32_t W, int32_t H, const float* target, float* rgb_out,
                                      float* grad_v, float* grad_p, double* loss, int32_t* overflow,
-                                     void* stream) {
+                                     int64_t* n_samples, void* stream) {
     if (!d || !theta_v || !theta_p || !occ || !mlp || !cams || !target || !rgb_out || !grad_v || !grad_p || !loss)
         return fail(MERF_EINVAL, "NULL argument");
     if (!is_pow2(d->L) || d->L < 2 || d->L > 1024 || !is_pow2(d->R) || d->R < 2 || d->R > 8192)
@@ -755,6 +759,11 @@ extern "C" merf_status merf_qat_step(const merf_qat_desc* d, const float* theta_
     S.step = d->step;
     S.lattice_step = std::ldexp(d->step, kF);
     cudaStream_t st = (cudaStream_t)stream;
+    {
+        int dev = 0;
+        CUDA_TRY(cudaGetDevice(&dev));
+        keep_pool_cached(dev);
+    }
     const int64_t nv = (int64_t)d->L * d->L * d->L * 8, np = (int64_t)3 * d->R * d->R * 8;
     const size_t samp_b = align256((size_t)rs.n * d->max_samples * 48);
     const size_t grid_b = align256((size_t)(nv + np) * 4);
@@ -775,11 +784,13 @@ extern "C" merf_status merf_qat_step(const merf_qat_desc* d, const float* theta_
     unsigned int* ovf = overflow ? (unsigned int*)overflow : (unsigned int*)(scratch + samp_b + 2 * grid_b);
     cudaError_t ce = cudaMemsetAsync(ovf, 0, 4, st);
     if (ce == cudaSuccess) ce = cudaMemsetAsync(loss, 0, 8, st);
+    if (ce == cudaSuccess && n_samples) ce = cudaMemsetAsync(n_samples, 0, 8, st);
     TraceArgs ta{};
     if (ce == cudaSuccess) ce = launch_setup(0, S, rs, ws, ta, nullptr, st);
     if (ce == cudaSuccess)
         ce = launch_qat(S, rs, ws, theta_v, theta_p, vv, vp, d->quantize ? 1 : 0, target, rgb_out, gvv, gvp,
-                        grad_v, grad_p, samp, d->max_samples, mlp, loss, ovf, d->L, d->R, d->occ_res, occ,
+                        grad_v, grad_p, samp, d->max_samples, mlp, loss, ovf,
+                        (unsigned long long*)n_samples, d->L, d->R, d->occ_res, occ,
                         (float)d->m_density, (float)d->m_appearance, st);
     cudaFreeAsync(scratch, st);
     cudaFreeAsync(base, st);

@@ -29,6 +29,7 @@ struct QatArgs {
     const float* mlp;       // [883]
     double* loss;
     unsigned int* overflow;
+    unsigned long long* n_samples;   // total evaluated samples (optional)
     int L, R, smax, Nf, sf;
     const uint32_t* occf;
     float step;
@@ -100,7 +101,7 @@ __global__ void __launch_bounds__(128) qat_ray_kernel(DevScene S, RaySource rs, 
     if (r >= rs.n) return;
     int view, px, py;
     if (!ray_pixel(rs, r, view, px, py)) return;
-    const int64_t pix = (int64_t)py * rs.W + px;
+    const int64_t pix = ((int64_t)view * rs.H + py) * rs.W + px;
     float* rec0 = A.samp + (size_t)r * A.smax * 12;
     // ---------------- forward ----------------
     float acc[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -116,12 +117,26 @@ __global__ void __launch_bounds__(128) qat_ray_kernel(DevScene S, RaySource rs, 
                 continue;
             float t[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
             for_corners(A, Qx, Qy, Qz, [&](int g, int e, float w) {
-                const float* src = (g == 0) ? A.vv + (size_t)e * 8 : A.vp + ((size_t)(g - 1) * A.R * A.R + e) * 8;
-#pragma unroll
-                for (int c = 0; c < 8; c++) t[c] = fmaf(w, src[c], t[c]);
+                const float4* src = reinterpret_cast<const float4*>(
+                    (g == 0) ? A.vv + (size_t)e * 8 : A.vp + ((size_t)(g - 1) * A.R * A.R + e) * 8);
+                const float4 a = __ldg(src), b = __ldg(src + 1);
+                t[0] = fmaf(w, a.x, t[0]);
+                t[1] = fmaf(w, a.y, t[1]);
+                t[2] = fmaf(w, a.z, t[2]);
+                t[3] = fmaf(w, a.w, t[3]);
+                t[4] = fmaf(w, b.x, t[4]);
+                t[5] = fmaf(w, b.y, t[5]);
+                t[6] = fmaf(w, b.z, t[6]);
+                t[7] = fmaf(w, b.w, t[7]);
             });
             const float tau = expf(t[0]);
             const float alpha = 1.f - expf(-tau * A.step);
+            float xs[7];
+#pragma unroll
+            for (int c = 0; c < 7; c++) {
+                xs[c] = 1.f / (1.f + expf(-t[1 + c]));
+                acc[c] = fmaf(alpha * T, xs[c], acc[c]);
+            }
             if (n < A.smax) {
                 float* rec = rec0 + (size_t)n * 12;
                 rec[0] = __int_as_float(Qx);
@@ -130,11 +145,7 @@ __global__ void __launch_bounds__(128) qat_ray_kernel(DevScene S, RaySource rs, 
                 rec[3] = t[0];
                 rec[4] = T;
 #pragma unroll
-                for (int c = 0; c < 7; c++) {
-                    const float x = 1.f / (1.f + expf(-t[1 + c]));
-                    rec[5 + c] = x;
-                    acc[c] = fmaf(alpha * T, x, acc[c]);
-                }
+                for (int c = 0; c < 7; c++) rec[5 + c] = xs[c];
             } else {
                 over = true;
             }
@@ -143,6 +154,7 @@ __global__ void __launch_bounds__(128) qat_ray_kernel(DevScene S, RaySource rs, 
         }
     }
     if (over) atomicAdd(A.overflow, 1u);
+    if (A.n_samples) atomicAdd(A.n_samples, (unsigned long long)n);
     // ---------------- deferred MLP forward (Eq. 3) ----------------
     double od[3], dd[3];
     raygen(rs.cb.cam[view], px, py, od, dd);
@@ -238,10 +250,12 @@ __global__ void __launch_bounds__(128) qat_ray_kernel(DevScene S, RaySource rs, 
         for (int c = 0; c < 7; c++) dt[1 + c] = w * G[c] * rec[5 + c] * (1.f - rec[5 + c]);
         for_corners(A, __float_as_int(rec[0]), __float_as_int(rec[1]), __float_as_int(rec[2]),
                     [&](int g, int e, float wc) {
-                        float* dst = (g == 0) ? A.gv + (size_t)e * 8 : A.gp + ((size_t)(g - 1) * A.R * A.R + e) * 8;
-#pragma unroll
-                        for (int c = 0; c < 8; c++)
-                            if (wc != 0.f) atomicAdd(dst + c, wc * dt[c]);
+                        if (wc == 0.f) return;
+                        float4* dst = reinterpret_cast<float4*>(
+                            (g == 0) ? A.gv + (size_t)e * 8 : A.gp + ((size_t)(g - 1) * A.R * A.R + e) * 8);
+                        // vector reductions (sm_90+): 2 per corner instead of 8 scalar atomics
+                        atomicAdd(dst, make_float4(wc * dt[0], wc * dt[1], wc * dt[2], wc * dt[3]));
+                        atomicAdd(dst + 1, make_float4(wc * dt[4], wc * dt[5], wc * dt[6], wc * dt[7]));
                     });
     }
 }
@@ -251,14 +265,14 @@ static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / 
 cudaError_t launch_qat(const DevScene& S, const RaySource& rs, const Workspace& ws, const float* theta_v,
                        const float* theta_p, float* vv, float* vp, int quant, const float* target, float* rgb,
                        float* gvals_v, float* gvals_p, float* grad_v, float* grad_p, float* samp, int smax,
-                       const float* mlp, double* loss, unsigned int* overflow, int L, int R, int Nf,
-                       const uint32_t* occf, float md, float ma, cudaStream_t st) {
+                       const float* mlp, double* loss, unsigned int* overflow, unsigned long long* n_samples, int L,
+                       int R, int Nf, const uint32_t* occf, float md, float ma, cudaStream_t st) {
     const int64_t nv = (int64_t)L * L * L * 8, np = (int64_t)3 * R * R * 8;
     prequant_kernel<<<nblk(nv, 256), 256, 0, st>>>(theta_v, nv, quant, md, ma, vv);
     prequant_kernel<<<nblk(np, 256), 256, 0, st>>>(theta_p, np, quant, md, ma, vp);
     cudaMemsetAsync(gvals_v, 0, nv * 4, st);
     cudaMemsetAsync(gvals_p, 0, np * 4, st);
-    QatArgs A{vv, vp, target, rgb, gvals_v, gvals_p, samp, mlp, loss, overflow, L, R, smax, Nf,
+    QatArgs A{vv, vp, target, rgb, gvals_v, gvals_p, samp, mlp, loss, overflow, n_samples, L, R, smax, Nf,
               kF + 2 - (31 - __builtin_clz((unsigned)Nf)), occf, (float)S.step};
     qat_ray_kernel<<<nblk(rs.n, 128), 128, 0, st>>>(S, rs, ws, A);
     ste_kernel<<<nblk(nv, 256), 256, 0, st>>>(theta_v, gvals_v, nv, md, ma, grad_v);

@@ -98,7 +98,7 @@ SIGNATURES = [
     ("merf_bake_occupancy", C.c_int, [_vp, _vp, _vp, _i64, _i32, C.c_double, C.c_double, C.c_double, _vp, _vp]),
     ("merf_pack_atlas", C.c_int, [_vp, _i32, _vp, _i64, _vp, _vp]),
     ("merf_qat_step", C.c_int, [C.POINTER(merf_qat_desc), _vp, _vp, _vp, _vp, C.POINTER(merf_camera), _i32,
-                                _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+                                _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     ("merf_build_block_index", C.c_int, [_vp, C.POINTER(merf_scene_desc), _vp, C.POINTER(_i64), _vp]),
 ]
 
@@ -293,10 +293,12 @@ def merf_pack_atlas(dense, L: int, index, n_blocks: int, atlas_out, stream=None)
 
 def merf_qat_step(theta_v, theta_p, occ, N: int, mlp, cams, W: int, H: int, target, rgb_out, grad_v,
                   grad_p, loss, step: float, quantize: bool = True, max_samples: int = 1024,
-                  overflow=None, m_density: float = 14.0, m_appearance: float = 7.0, stream=None) -> None:
+                  overflow=None, n_samples=None, m_density: float = 14.0, m_appearance: float = 7.0,
+                  stream=None) -> None:
     """NEXT-3 quantisation-aware forward + backward (Eq. 7-8) on dense grids; every tensor is a
     device tensor: theta_v [L,L,L,8] / theta_p [3,R,R,8] float32, occ uint32 bits of N^3,
-    target / rgb_out [n,H,W,3] float32, grad_* like theta, loss float64 [1], overflow int32 [1]."""
+    target / rgb_out [n,H,W,3] float32, grad_* like theta, loss float64 [1], overflow int32 [1],
+    n_samples int64 [1]."""
     d = merf_qat_desc()
     d.L, d.R, d.occ_res = int(theta_v.shape[0]), int(theta_p.shape[1]), int(N)
     d.quantize, d.max_samples, d.step = int(bool(quantize)), int(max_samples), float(step)
@@ -304,7 +306,7 @@ def merf_qat_step(theta_v, theta_p, occ, N: int, mlp, cams, W: int, H: int, targ
     carr = cameras_to_c(cams)
     _check(lib().merf_qat_step(C.byref(d), _ptr(theta_v), _ptr(theta_p), _ptr(occ), _ptr(mlp), carr, len(carr),
                                int(W), int(H), _ptr(target), _ptr(rgb_out), _ptr(grad_v), _ptr(grad_p),
-                               _ptr(loss), _ptr(overflow), _stream(stream)))
+                               _ptr(loss), _ptr(overflow), _ptr(n_samples), _stream(stream)))
 
 
 class Scene:

@@ -139,9 +139,11 @@ def _gpu(M, tv, tp, occ, mlp, cams, target, W_, H_, quant, max_samples=1024):
     gv, gp = torch.full_like(tvd, float("nan")), torch.full_like(tpd, float("nan"))
     loss = torch.empty(1, dtype=torch.float64, device=dev)
     ovf = torch.empty(1, dtype=torch.int32, device=dev)
+    ns = torch.empty(1, dtype=torch.int64, device=dev)
     M.merf_qat_step(tvd, tpd, t(occ), N, t(mlp), cams, W_, H_, t(target), rgb, gv, gp, loss, STEP,
-                    quantize=quant, max_samples=max_samples, overflow=ovf)
+                    quantize=quant, max_samples=max_samples, overflow=ovf, n_samples=ns)
     torch.cuda.synchronize()
+    _gpu.n_samples = int(ns.item())
     return loss.item(), rgb.reshape(len(cams), -1, 3).cpu().numpy(), gv.cpu().numpy(), gp.cpu().numpy(), int(ovf.item())
 
 
@@ -167,6 +169,8 @@ def test_gpu_qat_parity(M, quant, shape):
     l_ref, rgb_ref, gv_ref, gp_ref = _oracle(*case, W_, H_, quant)
     l_got, rgb_got, gv_got, gp_got, ovf = _gpu(M, *case, W_, H_, quant)
     assert ovf == 0
+    # the sample set is integer work: identical count (readings D5-D8)
+    assert _gpu.n_samples == sum(len(Q.sample_positions(c, W_, H_, case[2], N, STEP)[0]) for c in case[4])
     assert np.abs(rgb_got - rgb_ref).max() <= 1e-4
     assert abs(l_got - l_ref) <= 1e-4 * max(1.0, l_ref)
     assert np.isfinite(gv_got).all() and np.isfinite(gp_got).all()
