@@ -215,27 +215,20 @@ __device__ __forceinline__ bool occ_bit(const uint32_t* bits, int cx, int cy, in
     return (w >> (lin & 31)) & 1u;
 }
 
-// First k' >= 0 with Qa + k' U outside [lo, hi) along one axis, capped at K (exact: a float
-// estimate corrected with int32 products, which cannot overflow once capped at K).
+// First k' >= 0 with Qa + k' U outside [lo, hi) along one axis, capped at K.  Both signs
+// reduce to e = ceil(num / |U|) with num = hi - Qa (U > 0) or Qa - lo + 1 (U < 0), num >= 1
+// while the current sample is inside the cell; U = 0 gives +inf -> K.  The fp32 estimate is
+// within one of the exact quotient (relative error ~2^-21, e <= K < 2^21), so one branch-free
+// correction each way makes it exact; e |U| <= (K + 1) |U| < 2^31 (the segment's lattice
+// length) cannot overflow.
 __device__ __forceinline__ int exit_axis(int Qa, int U, int lo, int hi, int K) {
-    if (U > 0) {                                   // min e with Qa + e U >= hi
-        int num = hi - Qa;
-        float ef = ceilf(__fdividef((float)num, (float)U));
-        if (ef >= (float)K) return K;
-        int e = (int)ef;
-        while (e * U < num) e++;
-        while ((e - 1) * U >= num) e--;
-        return e;
-    } else {                                       // min e with Qa + e U < lo
-        int num = Qa - lo;
-        int a = -U;
-        float ef = floorf(__fdividef((float)num, (float)a)) + 1.f;
-        if (ef >= (float)K) return K;
-        int e = (int)ef;
-        while ((e - 1) * a > num) e--;
-        while (e * a <= num) e++;
-        return e;
-    }
+    const int a = abs(U);
+    const int num = U > 0 ? hi - Qa : Qa - lo + 1;
+    const float ef = ceilf(__fdividef((float)num, (float)a));
+    int e = (int)fminf(ef, (float)K);
+    e += (e * a < num) ? 1 : 0;
+    e -= ((e - 1) * a >= num) ? 1 : 0;
+    return min(e, K);
 }
 
 // texel coordinate on a grid of resolution M = 2^m (s = F + 2 - m): lower index, fraction

@@ -447,9 +447,9 @@ __global__ void __launch_bounds__(kMarchThreads, 4) march_kernel(DevScene S, int
                             // jump to the first lattice sample outside this empty cell (ray-AABB exit)
                             const int K = qa.w;
                             e = K;
-                            if (uu.x != 0) e = min(e, exit_axis(qa.x, uu.x, (cx << sh) - kTwoI, ((cx + 1) << sh) - kTwoI, K));
-                            if (uu.y != 0) e = min(e, exit_axis(qa.y, uu.y, (cy << sh) - kTwoI, ((cy + 1) << sh) - kTwoI, K));
-                            if (uu.z != 0) e = min(e, exit_axis(qa.z, uu.z, (cz << sh) - kTwoI, ((cz + 1) << sh) - kTwoI, K));
+                            e = min(e, exit_axis(qa.x, uu.x, (cx << sh) - kTwoI, ((cx + 1) << sh) - kTwoI, K));
+                            e = min(e, exit_axis(qa.y, uu.y, (cy << sh) - kTwoI, ((cy + 1) << sh) - kTwoI, K));
+                            e = min(e, exit_axis(qa.z, uu.z, (cz << sh) - kTwoI, ((cz + 1) << sh) - kTwoI, K));
                         }
                     }
                 }
