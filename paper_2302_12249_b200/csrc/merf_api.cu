@@ -120,6 +120,14 @@ static void fill_dev(merf_scene* s) {
     S.ka = (float)(2.0 * d.m_appearance / 255.0);
     S.md = d.m_density;
     S.ma = d.m_appearance;
+    {
+        const double l2e = 1.4426950408889634;
+        S.kd_l2 = (float)(2.0 * d.m_density / 255.0 * l2e);
+        S.md_l2 = (float)(d.m_density * l2e);
+        S.log2_step = (float)std::log2(d.step);
+        S.ka_l2n = (float)(-2.0 * d.m_appearance / 255.0 / 65535.0 * l2e);
+        S.ma_l2 = (float)(d.m_appearance * l2e);
+    }
     S.use_v = S.L > 0;
     for (int a = 0; a < 3; a++) S.use_p[a] = S.R > 0 && ((d.source_mask >> (1 + a)) & 1u);
     S.n_src = S.use_v + S.use_p[0] + S.use_p[1] + S.use_p[2];

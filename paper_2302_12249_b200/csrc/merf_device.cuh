@@ -37,6 +37,8 @@ struct DevScene {
     int sV, sP;                   // F + 2 - log2(L), F + 2 - log2(R)
     float kd, ka;                 // 2m/255 (density / appearance)
     float md, ma;                 // m (density / appearance)
+    float kd_l2, md_l2, log2_step;   // base-2 forms: log2(tau Delta) = s kd_l2 - n md_l2 + log2_step
+    float ka_l2n, ma_l2;          // sigmoid argument: -x log2e = acc ka_l2n + n ma_l2
     int n_src;                    // active sources (V counted only when L > 0)
     int use_v, use_p[3];
     double step;                  // Delta (power of two)
@@ -258,6 +260,18 @@ __device__ __forceinline__ void wsplit(uint32_t W, float f, uint32_t& w0, uint32
 }
 // pack two 16-bit weights into the (lo16, hi16) operand of dp2a
 __device__ __forceinline__ uint32_t wpack(uint32_t w0, uint32_t w1) { return w0 | (w1 << 16); }
+
+// MUFU-only exp2 / reciprocal (flush-to-zero; no range fix-up instructions)
+__device__ __forceinline__ float ex2_ftz(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float rcp_ftz(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 
 // byte k of w as an exact float (PRMT builds 2^23 + b, one FADD removes 2^23): no I2F
 __device__ __forceinline__ float byte_f(uint32_t w, int k) {

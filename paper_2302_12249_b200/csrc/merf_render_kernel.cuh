@@ -204,7 +204,6 @@ struct RayState {
     float F[4];
 };
 
-__device__ __forceinline__ float sigmoidf_(float x) { return __fdividef(1.0f, 1.0f + __expf(-x)); }
 
 // Appearance accumulation of a corner PAIR (texels a, b; 16-bit weights packed in wp):
 // integer dot products dp2a over byte pairs gathered with PRMT, 7 channels in 4 PRMT +
@@ -249,7 +248,7 @@ __device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, i
         }
         blk = bblk;
         if (blk >= 0) {
-            const uint2 oct = __ldg(S.vdens + ((size_t)blk * 512 + ((vi[2] & 7) * 8 + (vi[1] & 7)) * 8 + (vi[0] & 7)));
+            const uint2 oct = __ldg(S.vdens + (unsigned)(blk * 512 + ((vi[2] & 7) * 8 + (vi[1] & 7)) * 8 + (vi[0] & 7)));
             // trilinear as lerps (corner byte c = dx + 2 dy + 4 dz)
             const float b0 = byte_f(oct.x, 0), b1 = byte_f(oct.x, 1), b2 = byte_f(oct.x, 2), b3 = byte_f(oct.x, 3);
             const float b4 = byte_f(oct.y, 0), b5 = byte_f(oct.y, 1), b6 = byte_f(oct.y, 2), b7 = byte_f(oct.y, 3);
@@ -275,20 +274,22 @@ __device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, i
         if (!(ALL || S.use_p[a])) continue;
         const int ua = (a == 0) ? 1 : 0;
         const int va = (a == 2) ? 1 : 2;
-        const uint32_t quad = __ldg(S.pdens + ((size_t)a * S.R + pi[va]) * S.R + pi[ua]);
+        const uint32_t quad = __ldg(S.pdens + (unsigned)((a * S.R + pi[va]) * S.R + pi[ua]));
         const float fu = pf[ua], fv = pf[va];
         const float q0 = byte_f(quad, 0), q1 = byte_f(quad, 1), q2 = byte_f(quad, 2), q3 = byte_f(quad, 3);
         const float r0 = fmaf(fu, q1 - q0, q0), r1 = fmaf(fu, q3 - q2, q2);
         s0 += fmaf(fv, r1 - r0, r0);
     }
-    const float t0 = fmaf(s0, S.kd, -(float)n_src * S.md);
-    const float tau = __expf(t0);
-    const float alpha = 1.f - __expf(-tau * S.step_f);
+    // tau = exp(t0), t0 = s0 kd - n m (Eq. 6-7); alpha = 1 - exp(-tau Delta) in base 2:
+    // log2(tau Delta) = s0 kd log2e - n m log2e + log2 Delta (one FFMA), then two MUFU.EX2
+    const float tau_step = ex2_ftz(fmaf(s0, S.kd_l2, fmaf((float)n_src, -S.md_l2, S.log2_step)));
+    const float alpha = 1.f - ex2_ftz(tau_step * -1.4426950408889634f);
     if (alpha > S.alpha_skip) {
         // ---- appearance pass: 20 AoS texels, channels 1..7, 16-bit weights + dp2a
         uint32_t acc[7] = {0u, 0u, 0u, 0u, 0u, 0u, 0u};
         if (blk >= 0) {
-            const uint2* base = reinterpret_cast<const uint2*>(S.atlas + (size_t)blk * (729 * 8));
+            const uint2* atl = reinterpret_cast<const uint2*>(S.atlas);
+            const unsigned bbase = (unsigned)blk * 729u;   // < 2^21 * 729: 32-bit index math
             const int lx = vi[0] & 7, ly = vi[1] & 7, lz = vi[2] & 7;
             uint32_t wz[2], wzy[4];
             wsplit(65535u, vf[2], wz[0], wz[1]);
@@ -297,7 +298,7 @@ __device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, i
 #pragma unroll
             for (int c = 0; c < 4; c++) {                 // (dy, dz) rows; x pair per row
                 const int dy = c & 1, dz = c >> 1;
-                const uint2* row = base + ((lz + dz) * 9 + (ly + dy)) * 9 + lx;
+                const uint2* row = atl + (bbase + (unsigned)(((lz + dz) * 9 + (ly + dy)) * 9 + lx));
                 uint32_t w0, w1;
                 wsplit(wzy[c], vf[0], w0, w1);
                 acc_pair(acc, __ldg(row), __ldg(row + 1), wpack(w0, w1));
@@ -308,24 +309,26 @@ __device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, i
             if (!(ALL || S.use_p[a])) continue;
             const int ua = (a == 0) ? 1 : 0;
             const int va = (a == 2) ? 1 : 2;
-            const uint2* pl = reinterpret_cast<const uint2*>(S.planes) + (size_t)a * S.R * S.R;
+            const uint2* pl = reinterpret_cast<const uint2*>(S.planes);
             uint32_t wv[2];
             wsplit(65535u, pf[va], wv[0], wv[1]);
 #pragma unroll
             for (int dv = 0; dv < 2; dv++) {
-                const uint2* row = pl + (size_t)(pi[va] + dv) * S.R + pi[ua];
+                const uint2* row = pl + (unsigned)((a * S.R + pi[va] + dv) * S.R + pi[ua]);
                 uint32_t w0, w1;
                 wsplit(wv[dv], pf[ua], w0, w1);
                 acc_pair(acc, __ldg(row), __ldg(row + 1), wpack(w0, w1));
             }
         }
-        const float off = -(float)n_src * S.ma;
-        const float ka = S.ka * (1.f / 65535.f);
+        // sigmoid(x), x = acc ka / 65535 - n m: 1 / (1 + 2^(-x log2e)), the exponent in one FFMA
+        const float off = (float)n_src * S.ma_l2;
         const float w = alpha * st.T;
 #pragma unroll
-        for (int c = 0; c < 3; c++) st.cd[c] = fmaf(w, sigmoidf_(fmaf((float)(int)acc[c], ka, off)), st.cd[c]);
+        for (int c = 0; c < 3; c++)
+            st.cd[c] = fmaf(w, rcp_ftz(1.f + ex2_ftz(fmaf((float)(int)acc[c], S.ka_l2n, off))), st.cd[c]);
 #pragma unroll
-        for (int c = 0; c < 4; c++) st.F[c] = fmaf(w, sigmoidf_(fmaf((float)(int)acc[3 + c], ka, off)), st.F[c]);
+        for (int c = 0; c < 4; c++)
+            st.F[c] = fmaf(w, rcp_ftz(1.f + ex2_ftz(fmaf((float)(int)acc[3 + c], S.ka_l2n, off))), st.F[c]);
     } else if (ret == 0) {
         ret = 1;
     }
