@@ -1,0 +1,37 @@
+"""Write profiles/render_traffic.json (DRAM bytes per march launch, read by bench.py's
+roofline.traffic) from an `ncu --set full` capture of one march launch.
+
+  python tools/traffic_from_ncu.py report.ncu-rep [--out profiles/render_traffic.json]
+"""
+import argparse
+import csv
+import io
+import json
+import subprocess
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("report")
+    ap.add_argument("--out", default="profiles/render_traffic.json")
+    a = ap.parse_args()
+    out = subprocess.run(["ncu", "-i", a.report, "--page", "raw", "--csv", "--print-units", "base", "--metrics",
+                          "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum"],
+                         capture_output=True, text=True, check=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr = rows[0]
+    data = [r for r in rows[2:] if len(r) == len(hdr)]
+    r = dict(zip(hdr, data[0]))
+    rd, wr = float(r["dram__bytes_read.sum"]), float(r["dram__bytes_write.sum"])
+    d = {"source": f"{a.report.split('/')[-1]} (ncu --set full --clock-control none, {r['Kernel Name'].split('(')[0]},"
+                   " one launch = 8 views at 1080p, tools/prof_render.py --views 8)",
+         "dram_bytes_read_per_launch": rd, "dram_bytes_write_per_launch": wr, "dram_bytes_per_launch": rd + wr,
+         "ncu_duration_ns": float(r["gpu__time_duration.sum"]),
+         "note": "includes the workspace (segments read, accumulators written); scene texels hit L1/L2"}
+    with open(a.out, "w") as f:
+        json.dump(d, f, indent=1)
+    print(json.dumps(d))
+
+
+if __name__ == "__main__":
+    main()
