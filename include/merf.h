@@ -186,6 +186,24 @@ merf_status merf_render(const merf_scene *scene, const merf_camera *cams, int32_
 merf_status merf_kernel_times_get(merf_scene *scene, merf_kernel_times *out, int32_t reset);
 
 /*
+ * Progressive rendering ("the image is first rendered at a
+ * lower resolution ... additional low resolution images are rendered that are dynamically
+ * combined into the final high resolution image"): pass p in [0, stride^2) renders exactly
+ * the pixels (stride * i + p % stride, stride * j + p / stride) of every view -- each pixel
+ * with the same arithmetic as merf_render, so the stride^2 passes together write a frame
+ * identical to merf_render's -- into the full-resolution `out` (layout as merf_render);
+ * other pixels are left untouched unless `fill` != 0, which also writes each rendered colour
+ * to its stride x stride block (pixels (x, y) with x in [px, px + stride), y in [py, py +
+ * stride), clipped to the frame): the nearest-upsampled preview.  stride 1 = merf_render.
+ * A pass whose offset lies outside a tiny frame renders nothing.  MERF_COUNTERS is ignored.
+ * Asynchronous.  Errors: those of merf_render, MERF_EINVAL (stride not in [1, 64], pass not
+ * in [0, stride^2)).
+ */
+merf_status merf_render_progressive(const merf_scene *scene, const merf_camera *cams, int32_t n_cams,
+                                    int32_t W, int32_t H, int32_t stride, int32_t pass, int32_t fill,
+                                    int32_t format, void *out, uint32_t flags, void *stream);
+
+/*
  * End-to-end variant with HOST output: renders into scene-owned device staging buffers in
  * chunks and copies each finished chunk to `out_host` [host] (pinned memory recommended)
  * while the next chunk renders.  Synchronous on return.  Same layouts/errors as merf_render.

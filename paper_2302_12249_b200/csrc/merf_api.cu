@@ -462,15 +462,29 @@ static int march_flags(uint32_t flags, bool count) {
     return ((flags & MERF_DENSE) ? KF_DENSE : 0) | (count ? KF_COUNT : 0);
 }
 
+struct Progressive {
+    int stride, ox, oy, fill;
+};
+
 static merf_status render_frames(const merf_scene* s, const merf_camera* cams, int32_t n_cams,
                                  int32_t W, int32_t H, int32_t format, void* out, uint32_t flags,
-                                 cudaStream_t st, unsigned long long* d_stats) {
+                                 cudaStream_t st, unsigned long long* d_stats,
+                                 const Progressive* prog = nullptr) {
     const size_t px_bytes = format == MERF_RGBA_U8 ? 4 : 12;
     RaySource rs{};
     rs.W = W;
     rs.H = H;
-    rs.tiles_x = (W + 7) / 8;
-    rs.tiles_per_view = rs.tiles_x * ((H + 3) / 4);
+    int Wl = W, Hl = H;                    // pixel lattice covered by the rays
+    if (prog) {
+        rs.stride_m1 = prog->stride - 1;
+        rs.ox = prog->ox;
+        rs.oy = prog->oy;
+        rs.fill = prog->fill;
+        Wl = (W - prog->ox + prog->stride - 1) / prog->stride;
+        Hl = (H - prog->oy + prog->stride - 1) / prog->stride;
+    }
+    rs.tiles_x = (Wl + 7) / 8;
+    rs.tiles_per_view = rs.tiles_x * ((Hl + 3) / 4);
     const int64_t rays_per_view = (int64_t)rs.tiles_per_view * 32;
     int vpc = (int)(kChunkRays / rays_per_view);
     vpc = vpc < 1 ? 1 : (vpc > kViewsPerChunk ? kViewsPerChunk : vpc);
@@ -517,6 +531,18 @@ extern "C" merf_status merf_render(const merf_scene* s, const merf_camera* cams,
         if (stats) to_stats(h, stats);
     }
     return MERF_OK;
+}
+
+extern "C" merf_status merf_render_progressive(const merf_scene* s, const merf_camera* cams, int32_t n_cams,
+                                               int32_t W, int32_t H, int32_t stride, int32_t pass, int32_t fill,
+                                               int32_t format, void* out, uint32_t flags, void* stream) {
+    merf_status e = check_frames(s, cams, n_cams, W, H, format, out);
+    if (e) return e;
+    if (stride < 1 || stride > 64) return fail(MERF_EINVAL, "stride must be in [1, 64]");
+    if (pass < 0 || pass >= stride * stride) return fail(MERF_EINVAL, "pass must be in [0, stride^2)");
+    Progressive p{stride, pass % stride, pass / stride, fill ? 1 : 0};
+    if (p.ox >= W || p.oy >= H) return MERF_OK;   // an empty sub-lattice (frame smaller than stride)
+    return render_frames(s, cams, n_cams, W, H, format, out, flags, (cudaStream_t)stream, nullptr, &p);
 }
 
 extern "C" merf_status merf_render_host(const merf_scene* cs, const merf_camera* cams, int32_t n_cams,

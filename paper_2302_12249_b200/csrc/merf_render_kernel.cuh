@@ -58,6 +58,11 @@ struct RaySource {
     const double* d;
     const double* t_near;
     const int64_t* pixel_ids;    // trace / segments mode: pixel list of camera 0
+    // progressive rendering: the rays cover the sub-lattice of pixels
+    // (stride * i + ox, stride * j + oy); tiles_x / tiles_per_view count tiles of that
+    // lattice.  Zero-initialised = every pixel (stride 1).
+    int stride_m1, ox, oy;
+    int fill;                    // shade: also write the colour to the stride x stride block
 };
 
 __device__ __forceinline__ bool ray_pixel(const RaySource& rs, int64_t ray, int& view, int& px, int& py) {
@@ -66,8 +71,9 @@ __device__ __forceinline__ bool ray_pixel(const RaySource& rs, int64_t ray, int&
     view = (int)(tile / rs.tiles_per_view);
     const int tt = (int)(tile - (int64_t)view * rs.tiles_per_view);
     const int ty = tt / rs.tiles_x, tx = tt - ty * rs.tiles_x;
-    px = tx * 8 + (lane & 7);
-    py = ty * 4 + (lane >> 3);
+    const int lx = tx * 8 + (lane & 7), ly = ty * 4 + (lane >> 3);
+    px = lx * rs.stride_m1 + lx + rs.ox;
+    py = ly * rs.stride_m1 + ly + rs.oy;
     return px < rs.W && py < rs.H;
 }
 
@@ -673,12 +679,12 @@ __global__ void __launch_bounds__(kSetupThreads) shade_kernel(DevScene S, RaySou
     const int64_t ray = rs.ray0 + r;
     float d[3];
     int64_t out_idx;
+    int view = 0, px = 0, py = 0;
     if (KF & KF_RAYS) {
 #pragma unroll
         for (int q = 0; q < 3; q++) d[q] = (float)rs.d[3 * ray + q];
         out_idx = ray;
     } else {
-        int view, px, py;
         if (!ray_pixel(rs, ray, view, px, py)) return;
         double od[3], dd[3];
         raygen(rs.cb.cam[view], px, py, od, dd);
@@ -691,15 +697,27 @@ __global__ void __launch_bounds__(kSetupThreads) shade_kernel(DevScene S, RaySou
     float h[3];
     deferred_mlp(s_mlp, x7, d, h);
     const float c0 = __saturatef(a0.x + h[0]), c1 = __saturatef(a0.y + h[1]), c2 = __saturatef(a0.z + h[2]);
-    if (KF & KF_U8) {
-        reinterpret_cast<uchar4*>(out)[out_idx] =
-            make_uchar4((unsigned char)__float2int_rn(c0 * 255.f), (unsigned char)__float2int_rn(c1 * 255.f),
-                        (unsigned char)__float2int_rn(c2 * 255.f), 255);
-    } else {
-        float* o3 = reinterpret_cast<float*>(out) + 3 * out_idx;
-        o3[0] = c0;
-        o3[1] = c1;
-        o3[2] = c2;
+    auto put = [&](int64_t idx) {
+        if (KF & KF_U8) {
+            reinterpret_cast<uchar4*>(out)[idx] =
+                make_uchar4((unsigned char)__float2int_rn(c0 * 255.f), (unsigned char)__float2int_rn(c1 * 255.f),
+                            (unsigned char)__float2int_rn(c2 * 255.f), 255);
+        } else {
+            float* o3 = reinterpret_cast<float*>(out) + 3 * idx;
+            o3[0] = c0;
+            o3[1] = c1;
+            o3[2] = c2;
+        }
+    };
+    put(out_idx);
+    if (!(KF & KF_RAYS) && rs.fill) {
+        // progressive preview: nearest upsampling of the sub-lattice pixel to its
+        // stride x stride block (clipped to the frame)
+        const int sd = rs.stride_m1 + 1;
+        for (int dy = 0; dy < sd; dy++)
+            for (int dx = 0; dx < sd; dx++)
+                if ((dx | dy) != 0 && px + dx < rs.W && py + dy < rs.H)
+                    put(((int64_t)view * rs.H + py + dy) * rs.W + px + dx);
     }
 }
 

@@ -88,6 +88,8 @@ SIGNATURES = [
     ("merf_scene_block_index", C.c_int, [_vp, _vp, _vp]),
     ("merf_render", C.c_int, [_vp, C.POINTER(merf_camera), _i32, _i32, _i32, _i32, _vp, _u32, _vp,
                               C.POINTER(merf_stats)]),
+    ("merf_render_progressive", C.c_int, [_vp, C.POINTER(merf_camera), _i32, _i32, _i32, _i32, _i32, _i32, _i32,
+                                          _vp, _u32, _vp]),
     ("merf_render_host", C.c_int, [_vp, C.POINTER(merf_camera), _i32, _i32, _i32, _i32, _vp, _u32, _vp]),
     ("merf_render_rays", C.c_int, [_vp, _vp, _vp, _vp, _i64, _vp, _u32, _vp, C.POINTER(merf_stats)]),
     ("merf_trace", C.c_int, [_vp, C.POINTER(merf_camera), _i32, _vp, _i64, _i32, _vp, _vp, _vp, _u32,
@@ -226,6 +228,14 @@ def merf_render(handle, cams, W: int, H: int, out, fmt: int = MERF_RGB_F32, flag
     _check(lib().merf_render(handle, carr, len(carr), int(W), int(H), int(fmt), _ptr(out), int(flags),
                              _stream(stream), C.byref(st) if st is not None else None))
     return st.as_dict() if st is not None else None
+
+
+def merf_render_progressive(handle, cams, W: int, H: int, stride: int, pass_: int, out, fill: bool = False,
+                            fmt: int = MERF_RGB_F32, flags: int = 0, stream=None) -> None:
+    """Render pass `pass_` of stride x stride progressive rendering into `out`."""
+    carr = cameras_to_c(cams)
+    _check(lib().merf_render_progressive(handle, carr, len(carr), int(W), int(H), int(stride), int(pass_),
+                                         int(bool(fill)), int(fmt), _ptr(out), int(flags), _stream(stream)))
 
 
 def merf_render_host(handle, cams, W: int, H: int, out_host, fmt: int = MERF_RGBA_U8,
