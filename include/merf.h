@@ -57,7 +57,8 @@ typedef enum {
     MERF_ENOMEM = 2,     /* device allocation failed                                      */
     MERF_ECUDA = 3,      /* a CUDA runtime call or kernel launch failed                   */
     MERF_ENCCL = 4,      /* reserved (frame gather is done by the caller's process group) */
-    MERF_EMISMATCH = 5   /* scene arrays inconsistent (unsound block index, bad entries)  */
+    MERF_EMISMATCH = 5,  /* scene arrays inconsistent (unsound block index, bad entries)  */
+    MERF_EIO = 6         /* bundle / camera file missing, unreadable, malformed or corrupt */
 } merf_status;
 
 enum { MERF_RGB_F32 = 0, MERF_RGBA_U8 = 1 };
@@ -303,6 +304,59 @@ merf_status merf_bake_occupancy(const double *x, const double *tau, const double
  */
 merf_status merf_pack_atlas(const uint8_t *dense, int32_t L, const int32_t *index, int64_t n_blocks,
                             uint8_t *atlas_out, void *stream);
+
+/*
+ * Asset ingestion (Sec. 5.3, "we encode textures as PNGs";
+ * SPEC S:430-465 bundle layout).  A bundle is a directory:
+ *   manifest.txt  "merf_bundle 1", L, R, C, block_size 8, level_res (coarse -> fine),
+ *                 m_density, m_appearance, step (%.17g), t_min, alpha_skip, source_mask,
+ *                 n_blocks, "background none", mlp_dims 34 16 16 3, the 883 MLP weights in
+ *                 decimal (%.9g, exact for fp32), and "file <name> <bytes> <crc32 hex>" per
+ *                 payload;
+ *   plane<a>_{density,diffuse,features}.png (a = 0..2, if R > 0): lossless 8-bit gray / RGB
+ *                 / RGBA rasters R x R (channels 0 / 1-3 / 4-7 of [R][R][8]);
+ *   atlas_{density,diffuse,features}.png (if L > 0 and n_blocks > 0): the atlas as a Z-major
+ *                 stack of 9 x 9 slices (slice q = 9 b + z), 455 slices per raster row
+ *                 (<= 4095 px wide), same channel split;
+ *   block_index.bin (if L > 0): int32 little-endian [(L/8)^3];
+ *   occupancy<i>.bin: level i packed little-endian bits, bit k of byte n = cell 8n + k, x
+ *                 fastest, ceil(N^3/8) bytes; coarse levels = OR-pool of the
+ *                 finest.
+ *
+ * merf_bundle_write: write the host arrays of merf_scene_upload (block_index required when
+ * L > 0) into `dir` (created if missing; files overwritten).  Coarse occupancy levels are
+ * pooled from occ_finest.  Errors: MERF_EINVAL, MERF_EMISMATCH (an index entry outside
+ * [-1, n_blocks): payload/manifest mismatch refuses to write), MERF_EIO.
+ *
+ * merf_bundle_read: parse `dir`; desc and *n_blocks are always filled; when every array
+ * pointer is NULL the call only queries them, otherwise planes [3][R][R][8] (if R > 0),
+ * block_index and atlas [n_blocks][9][9][9][8] (if L > 0), occ_finest ((N^3+31)/32 words)
+ * and mlp [883] (host, caller-owned, sized from the query) are filled.  Every payload's size
+ * and CRC-32 are checked, every raster's dimensions against the manifest, every coarse
+ * level against the pool of the finest.  Errors: MERF_EINVAL, MERF_EIO (missing file,
+ * checksum / size / version mismatch, malformed manifest or PNG), MERF_EMISMATCH.
+ *
+ * merf_scene_load: merf_bundle_read + merf_scene_upload (synchronous).
+ */
+merf_status merf_bundle_write(const char *dir, const merf_scene_desc *desc, const uint8_t *planes,
+                              const int32_t *block_index, const uint8_t *atlas, int64_t n_blocks,
+                              const uint32_t *occ_finest, const float *mlp);
+merf_status merf_bundle_read(const char *dir, merf_scene_desc *desc, int64_t *n_blocks, uint8_t *planes,
+                             int32_t *block_index, uint8_t *atlas, uint32_t *occ_finest, float *mlp);
+merf_status merf_scene_load(const char *dir, int32_t device, merf_scene **out);
+
+/*
+ * Camera file: one camera per line, '#' comments and blank lines skipped,
+ * 20 numbers: W H fx fy cx cy r00 r01 r02 t0 r10 r11 r12 t1 r20 r21 r22 t2 near far
+ * (camera-to-world [R | t] row-major, OpenCV axes, reading D18; `near` becomes t_near; far
+ * must exceed near and is otherwise unused: rays end at the contracted scene boundary).
+ * cams [host] (max_cams entries) or NULL to count; widths / heights [host] or NULL.
+ * Errors: MERF_EINVAL (NULL path / n_cams, more than max_cams cameras), MERF_EIO (unreadable
+ * file; a malformed line, non-positive size or focal length, far <= near, or a rotation
+ * that is not orthonormal with det +1 -- the message names the line).
+ */
+merf_status merf_cameras_read(const char *path, merf_camera *cams, int32_t max_cams, int32_t *n_cams,
+                              int32_t *widths, int32_t *heights);
 
 /*
  * Quantisation-aware training step (Sec. 5.2, Eq. 7-8) on

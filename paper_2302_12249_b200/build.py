@@ -57,7 +57,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         for _, log in results:
             f.write(log)
     tmp = LIB + ".tmp"
-    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *[o for o, _ in results], "-lcudart"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *[o for o, _ in results], "-lcudart", "-lz"]
     subprocess.check_call(cmd)
     os.replace(tmp, LIB)
     return LIB

@@ -51,6 +51,11 @@ static merf_status fail(merf_status s, const char* fmt, ...) {
     return s;
 }
 
+merf_status merf_set_error(merf_status s, const char* msg) {   // for the other translation units
+    g_err = msg;
+    return s;
+}
+
 #define CUDA_TRY(expr)                                                                    \
     do {                                                                                  \
         cudaError_t _e = (expr);                                                          \

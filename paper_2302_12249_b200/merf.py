@@ -16,12 +16,12 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libmerf.so")
 
-MERF_OK, MERF_EINVAL, MERF_ENOMEM, MERF_ECUDA, MERF_ENCCL, MERF_EMISMATCH = range(6)
+MERF_OK, MERF_EINVAL, MERF_ENOMEM, MERF_ECUDA, MERF_ENCCL, MERF_EMISMATCH, MERF_EIO = range(7)
 MERF_RGB_F32, MERF_RGBA_U8 = 0, 1
 MERF_NO_EARLY_TERM, MERF_COUNTERS, MERF_DENSE, MERF_TIMED, MERF_SPHERICAL = 1, 2, 4, 8, 16
 MAX_LEVELS = 4
 
-_STATUS = {1: "MERF_EINVAL", 2: "MERF_ENOMEM", 3: "MERF_ECUDA", 4: "MERF_ENCCL", 5: "MERF_EMISMATCH"}
+_STATUS = {1: "MERF_EINVAL", 2: "MERF_ENOMEM", 3: "MERF_ECUDA", 4: "MERF_ENCCL", 5: "MERF_EMISMATCH", 6: "MERF_EIO"}
 
 
 class MerfError(RuntimeError):
@@ -101,6 +101,11 @@ SIGNATURES = [
     ("merf_pack_atlas", C.c_int, [_vp, _i32, _vp, _i64, _vp, _vp]),
     ("merf_qat_step", C.c_int, [C.POINTER(merf_qat_desc), _vp, _vp, _vp, _vp, C.POINTER(merf_camera), _i32,
                                 _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    ("merf_bundle_write", C.c_int, [C.c_char_p, C.POINTER(merf_scene_desc), _vp, _vp, _vp, _i64, _vp, _vp]),
+    ("merf_bundle_read", C.c_int, [C.c_char_p, C.POINTER(merf_scene_desc), C.POINTER(_i64), _vp, _vp, _vp, _vp,
+                                   _vp]),
+    ("merf_scene_load", C.c_int, [C.c_char_p, _i32, C.POINTER(_vp)]),
+    ("merf_cameras_read", C.c_int, [C.c_char_p, C.POINTER(merf_camera), _i32, C.POINTER(_i32), _vp, _vp]),
     ("merf_build_block_index", C.c_int, [_vp, C.POINTER(merf_scene_desc), _vp, C.POINTER(_i64), _vp]),
 ]
 
@@ -319,12 +324,83 @@ def merf_qat_step(theta_v, theta_p, occ, N: int, mlp, cams, W: int, H: int, targ
                                _ptr(loss), _ptr(overflow), _ptr(n_samples), _stream(stream)))
 
 
+def merf_bundle_write(directory: str, scene) -> None:
+    """Write the host arrays of `scene` (as for merf_scene_upload; block_index required when
+    L > 0) as a PNG bundle (Sec. 5.3)."""
+    desc = make_desc(scene)
+    planes = np.ascontiguousarray(scene.planes, np.uint8)
+    atlas = np.ascontiguousarray(scene.atlas, np.uint8)
+    bidx = np.ascontiguousarray(scene.block_index, np.int32)
+    occ = np.ascontiguousarray(scene.occ_finest, np.uint32)
+    mlp = np.ascontiguousarray(scene.mlp, np.float32)
+    n_blocks = int(atlas.shape[0]) if atlas.ndim else 0
+    _check(lib().merf_bundle_write(os.fsencode(directory), C.byref(desc), _ptr(planes) if planes.size else None,
+                                   _ptr(bidx) if bidx.size else None, _ptr(atlas) if atlas.size else None,
+                                   n_blocks, _ptr(occ), _ptr(mlp)))
+
+
+class BundleScene:
+    """host arrays read from a bundle; attributes as merf_scene_upload expects."""
+
+
+def merf_bundle_read(directory: str) -> BundleScene:
+    d = merf_scene_desc()
+    nb = _i64(0)
+    path = os.fsencode(directory)
+    _check(lib().merf_bundle_read(path, C.byref(d), C.byref(nb), None, None, None, None, None))
+    sc = BundleScene()
+    sc.L, sc.R, sc.C = d.L, d.R, d.C
+    sc.level_res = tuple(d.level_res[i] for i in range(d.n_levels))
+    sc.m_density, sc.m_appearance = d.m_density, d.m_appearance
+    sc.step, sc.t_min, sc.alpha_skip, sc.source_mask = d.step, d.t_min, d.alpha_skip, d.source_mask
+    n = int(nb.value)
+    Nf = sc.level_res[-1]
+    sc.planes = np.zeros((3, d.R, d.R, 8) if d.R else (0,), np.uint8)
+    sc.block_index = np.zeros(((d.L // 8) ** 3,) if d.L else (0,), np.int32)
+    sc.atlas = np.zeros((n, 9, 9, 9, 8), np.uint8)
+    sc.occ_finest = np.zeros((Nf ** 3 + 31) // 32, np.uint32)
+    sc.mlp = np.zeros(883, np.float32)
+    _check(lib().merf_bundle_read(path, C.byref(d), C.byref(nb), _ptr(sc.planes) if sc.planes.size else None,
+                                  _ptr(sc.block_index) if sc.block_index.size else None,
+                                  _ptr(sc.atlas) if sc.atlas.size else None, _ptr(sc.occ_finest), _ptr(sc.mlp)))
+    return sc
+
+
+def merf_scene_load(directory: str, device: int = 0) -> int:
+    """read a bundle and upload it; returns the scene handle."""
+    h = C.c_void_p()
+    _check(lib().merf_scene_load(os.fsencode(directory), int(device), C.byref(h)))
+    return h.value
+
+
+def merf_cameras_read(path: str):
+    """-> (cams float64 [n, 17] as merf_camera, widths int32 [n], heights int32 [n])."""
+    n = _i32(0)
+    p = os.fsencode(path)
+    _check(lib().merf_cameras_read(p, None, 0, C.byref(n), None, None))
+    k = int(n.value)
+    arr = (merf_camera * max(k, 1))()
+    w = np.zeros(max(k, 1), np.int32)
+    h = np.zeros(max(k, 1), np.int32)
+    _check(lib().merf_cameras_read(p, arr, k, C.byref(n), _ptr(w), _ptr(h)))
+    cams = np.frombuffer(bytes(arr), np.float64).reshape(-1, 17)[:k].copy()
+    return cams, w[:k], h[:k]
+
+
 class Scene:
     """RAII wrapper of a device scene handle."""
 
     def __init__(self, scene, device: int = 0, canonical: bool = False):
         self.handle = merf_scene_upload(scene, device=device, canonical=canonical)
         self.device = device
+
+    @classmethod
+    def load(cls, directory: str, device: int = 0) -> "Scene":
+        """a scene from a PNG bundle (merf_scene_load)."""
+        self = cls.__new__(cls)
+        self.handle = merf_scene_load(directory, device)
+        self.device = device
+        return self
 
     def info(self) -> dict:
         return merf_scene_info_get(self.handle)
