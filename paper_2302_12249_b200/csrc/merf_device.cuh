@@ -246,20 +246,24 @@ __device__ __forceinline__ void texel(int Q, int s, int M, int& i0, float& f) {
 
 // 16-bit fixed-point interpolation weights that partition 65535 EXACTLY (so a constant
 // field interpolates exactly): split an integer weight W along one axis with fraction f
-// into (W - round(f W), round(f W)).  Rounding via the 1.5 * 2^23 magic (x + M leaves
-// round(x) in the low mantissa bits; no F2I), int -> float via the 2^23 magic (no I2F).
-__device__ __forceinline__ uint32_t rnd_u16(float x) {          // x in [0, 65535]
-    return __float_as_uint(x + 12582912.f) & 0xFFFFu;
+// into (W - round(f W), round(f W)).  The rounding is one FFMA against the 1.5 * 2^23 magic
+// (t = f W + M leaves round(f W) in the low mantissa bits: no F2I), and every weight is
+// carried both as an int and as an exact float so the next split needs no conversion.
+constexpr float kMagicF = 12582912.f;          // 1.5 * 2^23
+constexpr uint32_t kMagicBits = 0x4B400000u;   // its bit pattern (low 22 bits zero)
+__device__ __forceinline__ void wsplit(uint32_t Wi, float Wf, float f, uint32_t& w0i, float& w0f, uint32_t& w1i,
+                                       float& w1f) {
+    const float t = fmaf(f, Wf, kMagicF);
+    w1i = __float_as_uint(t) - kMagicBits;
+    w0i = Wi - w1i;
+    w1f = t - kMagicF;
+    w0f = Wf - w1f;
 }
-__device__ __forceinline__ float u2f(uint32_t v) {               // v < 2^23, exact
-    return __uint_as_float(0x4B000000u | v) - 8388608.f;
+// the last split, packed as the (lo16, hi16) = (W - w1, w1) operand of dp2a: FFMA, IADD3, PRMT
+__device__ __forceinline__ uint32_t wleaf(uint32_t Wi, float Wf, float f) {
+    const uint32_t t = __float_as_uint(fmaf(f, Wf, kMagicF));   // kMagicBits + w1
+    return __byte_perm(Wi + kMagicBits - t, t, 0x5410);
 }
-__device__ __forceinline__ void wsplit(uint32_t W, float f, uint32_t& w0, uint32_t& w1) {
-    w1 = rnd_u16(f * u2f(W));
-    w0 = W - w1;
-}
-// pack two 16-bit weights into the (lo16, hi16) operand of dp2a
-__device__ __forceinline__ uint32_t wpack(uint32_t w0, uint32_t w1) { return w0 | (w1 << 16); }
 
 // MUFU-only exp2 / reciprocal (flush-to-zero; no range fix-up instructions)
 __device__ __forceinline__ float ex2_ftz(float x) {

@@ -297,17 +297,16 @@ __device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, i
             const uint2* atl = reinterpret_cast<const uint2*>(S.atlas);
             const unsigned bbase = (unsigned)blk * 729u;   // < 2^21 * 729: 32-bit index math
             const int lx = vi[0] & 7, ly = vi[1] & 7, lz = vi[2] & 7;
-            uint32_t wz[2], wzy[4];
-            wsplit(65535u, vf[2], wz[0], wz[1]);
-            wsplit(wz[0], vf[1], wzy[0], wzy[1]);
-            wsplit(wz[1], vf[1], wzy[2], wzy[3]);
+            uint32_t zi[2], yi[4];
+            float zf[2], yf[4];
+            wsplit(65535u, 65535.f, vf[2], zi[0], zf[0], zi[1], zf[1]);
+            wsplit(zi[0], zf[0], vf[1], yi[0], yf[0], yi[1], yf[1]);
+            wsplit(zi[1], zf[1], vf[1], yi[2], yf[2], yi[3], yf[3]);
 #pragma unroll
             for (int c = 0; c < 4; c++) {                 // (dy, dz) rows; x pair per row
                 const int dy = c & 1, dz = c >> 1;
                 const uint2* row = atl + (bbase + (unsigned)(((lz + dz) * 9 + (ly + dy)) * 9 + lx));
-                uint32_t w0, w1;
-                wsplit(wzy[c], vf[0], w0, w1);
-                acc_pair(acc, __ldg(row), __ldg(row + 1), wpack(w0, w1));
+                acc_pair(acc, __ldg(row), __ldg(row + 1), wleaf(yi[c], yf[c], vf[0]));
             }
         }
 #pragma unroll
@@ -316,14 +315,13 @@ __device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, i
             const int ua = (a == 0) ? 1 : 0;
             const int va = (a == 2) ? 1 : 2;
             const uint2* pl = reinterpret_cast<const uint2*>(S.planes);
-            uint32_t wv[2];
-            wsplit(65535u, pf[va], wv[0], wv[1]);
+            uint32_t vi2[2];
+            float vf2[2];
+            wsplit(65535u, 65535.f, pf[va], vi2[0], vf2[0], vi2[1], vf2[1]);
 #pragma unroll
             for (int dv = 0; dv < 2; dv++) {
                 const uint2* row = pl + (unsigned)((a * S.R + pi[va] + dv) * S.R + pi[ua]);
-                uint32_t w0, w1;
-                wsplit(wv[dv], pf[ua], w0, w1);
-                acc_pair(acc, __ldg(row), __ldg(row + 1), wpack(w0, w1));
+                acc_pair(acc, __ldg(row), __ldg(row + 1), wleaf(vi2[dv], vf2[dv], pf[ua]));
             }
         }
         // sigmoid(x), x = acc ka / 65535 - n m: 1 / (1 + 2^(-x log2e)), the exponent in one FFMA
