@@ -128,6 +128,7 @@ static void fill_dev(merf_scene* s) {
     {
         const double l2e = 1.4426950408889634;
         S.kd_l2 = (float)(2.0 * d.m_density / 255.0 * l2e);
+        S.kd_l2w = (float)(2.0 * d.m_density / 255.0 * l2e / 65535.0);
         S.md_l2 = (float)(d.m_density * l2e);
         S.log2_step = (float)std::log2(d.step);
         S.ka_l2n = (float)(-2.0 * d.m_appearance / 255.0 / 65535.0 * l2e);

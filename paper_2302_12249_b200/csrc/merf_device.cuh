@@ -38,6 +38,7 @@ struct DevScene {
     float kd, ka;                 // 2m/255 (density / appearance)
     float md, ma;                 // m (density / appearance)
     float kd_l2, md_l2, log2_step;   // base-2 forms: log2(tau Delta) = s kd_l2 - n md_l2 + log2_step
+    float kd_l2w;                 // kd_l2 / 65535 (density sum in 16-bit weight units)
     float ka_l2n, ma_l2;          // sigmoid argument: -x log2e = acc ka_l2n + n ma_l2
     int n_src;                    // active sources (V counted only when L > 0)
     int use_v, use_p[3];
@@ -275,11 +276,6 @@ __device__ __forceinline__ float rcp_ftz(float x) {
     float y;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
-}
-
-// byte k of w as an exact float (PRMT builds 2^23 + b, one FADD removes 2^23): no I2F
-__device__ __forceinline__ float byte_f(uint32_t w, int k) {
-    return __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7440u | (unsigned)k)) - 8388608.f;
 }
 
 }  // namespace merf

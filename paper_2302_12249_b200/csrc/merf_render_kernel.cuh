@@ -238,13 +238,16 @@ __device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, i
     const bool use_v = ALL || S.use_v;
     const int Q[3] = {Qx, Qy, Qz};
     int ret = 0;
-    // ---- density pass: 1 octet (V) + 3 quads (planes)
+    // Interpolation weights, computed once and shared by both passes: 16-bit fixed point,
+    // partitioning 65535 exactly per source, packed per corner pair for dp2a.  V: rows
+    // (dy, dz), c = dy + 2 dz, x pair per row; plane a: rows dv, u pair per row.
     int n_src = ALL ? 4 : S.n_src;
-    float s0 = 0.f;
+    uint32_t sd = 0u;                  // density sum over sources, units of 1/65535 byte
     int vi[3] = {0, 0, 0};
-    float vf[3] = {0.f, 0.f, 0.f};
+    uint32_t wV[4] = {0u, 0u, 0u, 0u};
     int blk = -1;
     if (use_v) {
+        float vf[3];
 #pragma unroll
         for (int a = 0; a < 3; a++) texel(Q[a], S.sV, S.L, vi[a], vf[a]);
         const int slot = ((vi[2] >> 3) * S.nb + (vi[1] >> 3)) * S.nb + (vi[0] >> 3);
@@ -253,15 +256,20 @@ __device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, i
             bblk = __ldg(S.block_index + slot);
         }
         blk = bblk;
+        uint32_t zi[2], yi[4];
+        float zf[2], yf[4];
+        wsplit(65535u, 65535.f, vf[2], zi[0], zf[0], zi[1], zf[1]);
+        wsplit(zi[0], zf[0], vf[1], yi[0], yf[0], yi[1], yf[1]);
+        wsplit(zi[1], zf[1], vf[1], yi[2], yf[2], yi[3], yf[3]);
+#pragma unroll
+        for (int c = 0; c < 4; c++) wV[c] = wleaf(yi[c], yf[c], vf[0]);
         if (blk >= 0) {
+            // ---- density pass, V: the corner octet (byte c = dx + 2 dy + 4 dz) as 4 dp2a
             const uint2 oct = __ldg(S.vdens + (unsigned)(blk * 512 + ((vi[2] & 7) * 8 + (vi[1] & 7)) * 8 + (vi[0] & 7)));
-            // trilinear as lerps (corner byte c = dx + 2 dy + 4 dz)
-            const float b0 = byte_f(oct.x, 0), b1 = byte_f(oct.x, 1), b2 = byte_f(oct.x, 2), b3 = byte_f(oct.x, 3);
-            const float b4 = byte_f(oct.y, 0), b5 = byte_f(oct.y, 1), b6 = byte_f(oct.y, 2), b7 = byte_f(oct.y, 3);
-            const float x00 = fmaf(vf[0], b1 - b0, b0), x10 = fmaf(vf[0], b3 - b2, b2);
-            const float x01 = fmaf(vf[0], b5 - b4, b4), x11 = fmaf(vf[0], b7 - b6, b6);
-            const float y0 = fmaf(vf[1], x10 - x00, x00), y1 = fmaf(vf[1], x11 - x01, x01);
-            s0 = fmaf(vf[2], y1 - y0, y0);
+            sd = __dp2a_lo(wV[0], oct.x, sd);
+            sd = __dp2a_hi(wV[1], oct.x, sd);
+            sd = __dp2a_lo(wV[2], oct.y, sd);
+            sd = __dp2a_hi(wV[3], oct.y, sd);
         } else {
             n_src -= 1;                    // a missing block contributes nothing
             ret = 2;
@@ -269,44 +277,44 @@ __device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, i
     }
     // plane texel coordinates: each axis feeds two planes (P_x(y,z), P_y(x,z), P_z(x,y))
     int pi[3] = {0, 0, 0};
-    float pf[3] = {0.f, 0.f, 0.f};
+    uint32_t wP[3][2] = {{0u, 0u}, {0u, 0u}, {0u, 0u}};
     const bool any_p = ALL || S.R > 0;
     if (any_p) {
+        float pf[3];
 #pragma unroll
         for (int a = 0; a < 3; a++) texel(Q[a], S.sP, S.R, pi[a], pf[a]);
-    }
 #pragma unroll
-    for (int a = 0; a < 3; a++) {
-        if (!(ALL || S.use_p[a])) continue;
-        const int ua = (a == 0) ? 1 : 0;
-        const int va = (a == 2) ? 1 : 2;
-        const uint32_t quad = __ldg(S.pdens + (unsigned)((a * S.R + pi[va]) * S.R + pi[ua]));
-        const float fu = pf[ua], fv = pf[va];
-        const float q0 = byte_f(quad, 0), q1 = byte_f(quad, 1), q2 = byte_f(quad, 2), q3 = byte_f(quad, 3);
-        const float r0 = fmaf(fu, q1 - q0, q0), r1 = fmaf(fu, q3 - q2, q2);
-        s0 += fmaf(fv, r1 - r0, r0);
+        for (int a = 0; a < 3; a++) {
+            if (!(ALL || S.use_p[a])) continue;
+            const int ua = (a == 0) ? 1 : 0;
+            const int va = (a == 2) ? 1 : 2;
+            uint32_t v0i, v1i;
+            float v0f, v1f;
+            wsplit(65535u, 65535.f, pf[va], v0i, v0f, v1i, v1f);
+            wP[a][0] = wleaf(v0i, v0f, pf[ua]);
+            wP[a][1] = wleaf(v1i, v1f, pf[ua]);
+            // ---- density pass, plane a: the texel quad (byte du + 2 dv) as 2 dp2a
+            const uint32_t quad = __ldg(S.pdens + (unsigned)((a * S.R + pi[va]) * S.R + pi[ua]));
+            sd = __dp2a_lo(wP[a][0], quad, sd);
+            sd = __dp2a_hi(wP[a][1], quad, sd);
+        }
     }
-    // tau = exp(t0), t0 = s0 kd - n m (Eq. 6-7); alpha = 1 - exp(-tau Delta) in base 2:
-    // log2(tau Delta) = s0 kd log2e - n m log2e + log2 Delta (one FFMA), then two MUFU.EX2
-    const float tau_step = ex2_ftz(fmaf(s0, S.kd_l2, fmaf((float)n_src, -S.md_l2, S.log2_step)));
+    // tau = exp(t0), t0 = s0 kd - n m (Eq. 6-7), s0 = sd / 65535; alpha = 1 - exp(-tau Delta)
+    // in base 2: log2(tau Delta) = sd kd log2e / 65535 - n m log2e + log2 Delta (one FFMA)
+    const float tau_step = ex2_ftz(fmaf((float)(int)sd, S.kd_l2w, fmaf((float)n_src, -S.md_l2, S.log2_step)));
     const float alpha = 1.f - ex2_ftz(tau_step * -1.4426950408889634f);
     if (alpha > S.alpha_skip) {
-        // ---- appearance pass: 20 AoS texels, channels 1..7, 16-bit weights + dp2a
+        // ---- appearance pass: 20 AoS texels, channels 1..7, the same weights + dp2a
         uint32_t acc[7] = {0u, 0u, 0u, 0u, 0u, 0u, 0u};
         if (blk >= 0) {
             const uint2* atl = reinterpret_cast<const uint2*>(S.atlas);
             const unsigned bbase = (unsigned)blk * 729u;   // < 2^21 * 729: 32-bit index math
             const int lx = vi[0] & 7, ly = vi[1] & 7, lz = vi[2] & 7;
-            uint32_t zi[2], yi[4];
-            float zf[2], yf[4];
-            wsplit(65535u, 65535.f, vf[2], zi[0], zf[0], zi[1], zf[1]);
-            wsplit(zi[0], zf[0], vf[1], yi[0], yf[0], yi[1], yf[1]);
-            wsplit(zi[1], zf[1], vf[1], yi[2], yf[2], yi[3], yf[3]);
 #pragma unroll
             for (int c = 0; c < 4; c++) {                 // (dy, dz) rows; x pair per row
                 const int dy = c & 1, dz = c >> 1;
                 const uint2* row = atl + (bbase + (unsigned)(((lz + dz) * 9 + (ly + dy)) * 9 + lx));
-                acc_pair(acc, __ldg(row), __ldg(row + 1), wleaf(yi[c], yf[c], vf[0]));
+                acc_pair(acc, __ldg(row), __ldg(row + 1), wV[c]);
             }
         }
 #pragma unroll
@@ -315,13 +323,10 @@ __device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, i
             const int ua = (a == 0) ? 1 : 0;
             const int va = (a == 2) ? 1 : 2;
             const uint2* pl = reinterpret_cast<const uint2*>(S.planes);
-            uint32_t vi2[2];
-            float vf2[2];
-            wsplit(65535u, 65535.f, pf[va], vi2[0], vf2[0], vi2[1], vf2[1]);
 #pragma unroll
             for (int dv = 0; dv < 2; dv++) {
                 const uint2* row = pl + (unsigned)((a * S.R + pi[va] + dv) * S.R + pi[ua]);
-                acc_pair(acc, __ldg(row), __ldg(row + 1), wleaf(vi2[dv], vf2[dv], pf[ua]));
+                acc_pair(acc, __ldg(row), __ldg(row + 1), wP[a][dv]);
             }
         }
         // sigmoid(x), x = acc ka / 65535 - n m: 1 / (1 + 2^(-x log2e)), the exponent in one FFMA

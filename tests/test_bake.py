@@ -155,8 +155,14 @@ def test_gpu_bake_to_render_chain():
     s = M.Scene(sc, canonical=True)
     cams, W, H = config_cameras("c1")
     out, st = s.render(cams, W, H, stats=True)
+    # the sample set is integer work: compare its size without early termination (the
+    # T < t_min stop is a float decision, fp32 here vs fp64 in the oracle; reading D19)
+    _, st_all = s.render(cams, W, H, flags=M.MERF_NO_EARLY_TERM, stats=True)
     torch.cuda.synchronize()
-    ref = O.render(O.OracleScene(sc), cams[0], W, H)
-    assert st["evaluated"] == ref["stats"]["evaluated"] and st["missing_blocks"] == 0
+    osc = O.OracleScene(sc)
+    ref = O.render(osc, cams[0], W, H)
+    ref_all = O.render(osc, cams[0], W, H, flags=O.NO_EARLY_TERM)
+    assert st_all["evaluated"] == ref_all["stats"]["evaluated"] and st["missing_blocks"] == 0
+    assert abs(st["evaluated"] - ref["stats"]["evaluated"]) <= 1e-3 * ref["stats"]["evaluated"]
     assert np.abs(out[0].reshape(-1, 3).cpu().numpy() - ref["rgb"]).max() <= 2e-3
     s.close()

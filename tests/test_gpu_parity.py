@@ -56,9 +56,26 @@ def _gpu_trace(M, sc, cam, W, pixels, max_per_ray=2048, flags=0):
     return cells.cpu().numpy().view(np.uint64), T.cpu().numpy(), cnt.cpu().numpy()
 
 
+# GPU density with 16-bit exact-partition weights (GPU numerical choices):
+# |dt0| <= 24 * 127.5 / 65535 * 2m/255 = 0.0051 (m = 14), so optical depth agrees to
+# OD_REL = 0.52 % relative (+ fp32 slack), and T at the termination cut (OD = ln 5000) to
+# T_CUT_REL = exp(0.0052 * ln 5000) - 1 = 4.5 % (reading D19).
+OD_REL = 0.0052
+T_CUT_REL = 0.045
+
+
+def _close_transmittance(Tg, To):
+    """GPU vs oracle transmittance after each sample, within the optical-depth bound."""
+    Tg, To = np.asarray(Tg, np.float64), np.asarray(To, np.float64)
+    live = To > 1e-5
+    odg, odo = -np.log(np.maximum(Tg[live], 1e-30)), -np.log(To[live])
+    ok = np.all(np.abs(odg - odo) <= OD_REL * odo + 2e-5)
+    return ok and np.all(Tg[~live] <= 2e-5)
+
+
 def _compare_traces(g, o, T_oracle=None, t_min=2e-4):
     """bit-exact visited cells; with termination on, a length may differ only when the
-    oracle's transmittance at the cut is within 1e-4 relative of t_min (reading D19)."""
+    oracle's transmittance at the cut is within T_CUT_REL of t_min (reading D19)."""
     gc, gT, gn = g
     oc, on = o["trace_cells"], o["trace_count"]
     mism = 0
@@ -69,7 +86,7 @@ def _compare_traces(g, o, T_oracle=None, t_min=2e-4):
             mism += 1
             k = min(gn[r], on[r]) - 1
             Tcut = o["trace_T"][r, k]
-            assert abs(Tcut - t_min) <= 1e-4 * t_min * 10, (r, gn[r], on[r], Tcut)
+            assert abs(Tcut - t_min) <= T_CUT_REL * t_min, (r, gn[r], on[r], Tcut)
     return mism
 
 
@@ -192,10 +209,10 @@ def test_c1_traces_bit_exact(M, c1_scene, flags):
     mism = _compare_traces(g, o)
     if flags == 1:
         assert mism == 0 and np.array_equal(g[2], o["trace_count"])
-    # transmittance after each sample agrees in fp32
+    # transmittance after each sample agrees within the optical-depth bound
     n = np.minimum(g[2], o["trace_count"])
     for r in range(0, W * H, 7):
-        assert np.allclose(g[1][r, :n[r]], o["trace_T"][r, :n[r]], atol=2e-5, rtol=1e-4)
+        assert _close_transmittance(g[1][r, :n[r]], o["trace_T"][r, :n[r]]), r
 
 
 def test_dense_equals_hierarchical_on_gpu(M, c1_scene):
@@ -233,8 +250,9 @@ def test_random_scenes(M, seed, mask, WH):
     cams = np.stack([look_at_camera(rng.uniform(-1.5, 1.5, 3), target=rng.uniform(-0.5, 0.5, 3),
                                     W=W, H=H, fov_x_deg=70) for _ in range(3)])
     got, st = _gpu_frame(M, sc, cams, W, H)
+    _, st_all = _gpu_frame(M, sc, cams, W, H, flags=M.MERF_NO_EARLY_TERM)
     osc = O.OracleScene(sc)
-    ev = 0
+    ev, ev_all = 0, 0
     for c in range(3):
         ref = O.render(osc, cams[c], W, H)
         g = got[c].reshape(-1, 3)
@@ -244,7 +262,10 @@ def test_random_scenes(M, seed, mask, WH):
         gt = _gpu_trace(M, sc, cams[c], W, np.arange(W * H), 2048, flags=M.MERF_NO_EARLY_TERM)
         assert np.array_equal(gt[2], o["trace_count"])
         assert np.array_equal(gt[0], o["trace_cells"])
-    assert st["evaluated"] == ev
+        ev_all += int(o["trace_count"].sum())
+    # the sample set is integer work (exact); the T < t_min cut is a float decision (D19)
+    assert st_all["evaluated"] == ev_all
+    assert abs(st["evaluated"] - ev) <= 1e-3 * ev
 
 
 def test_empty_occupancy(M):
