@@ -108,6 +108,8 @@ typedef struct {
     int64_t skips;              /* empty-cell jumps                                   */
     int64_t missing_blocks;     /* evaluated samples whose V block is absent (must be 0)      */
     int64_t region_segments[7]; /* kept segments per region (core, +x, -x, +y, -y, +z, -z)   */
+    int64_t march_rounds;       /* warp shading rounds of the persistent march (perf counter) */
+    int64_t march_steps;        /* warp traversal iterations (perf counter)                   */
 } merf_stats;
 
 typedef struct {

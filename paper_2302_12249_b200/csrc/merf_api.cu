@@ -355,6 +355,8 @@ static void to_stats(const unsigned long long* h, merf_stats* st) {
     st->skips = (int64_t)h[4];
     st->missing_blocks = (int64_t)h[5];
     for (int g = 0; g < 7; g++) st->region_segments[g] = (int64_t)h[6 + g];
+    st->march_rounds = (int64_t)h[13];
+    st->march_steps = (int64_t)h[14];
 }
 
 // ------------------------------------------------------------------------------------

@@ -372,7 +372,7 @@ __global__ void __launch_bounds__(kMarchThreads, 4) march_kernel(DevScene S, int
     st.T = 1.f;
     st.cd[0] = st.cd[1] = st.cd[2] = 0.f;
     st.F[0] = st.F[1] = st.F[2] = st.F[3] = 0.f;
-    int c_eval = 0, c_donly = 0, c_skip = 0, c_miss = 0;
+    int c_eval = 0, c_donly = 0, c_skip = 0, c_miss = 0, c_rounds = 0, c_steps = 0;
 
     auto finish = [&]() {
         float4* a = ws.accum + (int64_t)ray * 2;
@@ -421,6 +421,7 @@ __global__ void __launch_bounds__(kMarchThreads, 4) march_kernel(DevScene S, int
             const bool want = ray >= 0 && !found;
             const unsigned m_want = __ballot_sync(FULL, want);
             if (m_want == 0) break;
+            if (KF & KF_COUNT) c_steps += lane == 0;
             if (it > 0 && __popc(act & ~m_want) >= tune.shade_min) break;   // lanes ready to shade
             if (!want) continue;
             if (k >= qa.w) {                                  // segment exhausted
@@ -475,6 +476,7 @@ __global__ void __launch_bounds__(kMarchThreads, 4) march_kernel(DevScene S, int
         }
 
         // ---------------- shading (converged) ----------------
+        if (KF & KF_COUNT) c_rounds += (lane == 0 && __any_sync(FULL, found));
         if (found) {
             last_cell = fcell;
             const int kind = shade_sample<KF>(S, Qx, Qy, Qz, st, bslot, bblk);
@@ -500,6 +502,8 @@ __global__ void __launch_bounds__(kMarchThreads, 4) march_kernel(DevScene S, int
         add_stat(stats, 3, c_donly);
         add_stat(stats, 4, c_skip);
         add_stat(stats, 5, c_miss);
+        add_stat(stats, 13, c_rounds);
+        add_stat(stats, 14, c_steps);
     }
 }
 
