@@ -476,7 +476,10 @@ __global__ void __launch_bounds__(kMarchThreads, 4) march_kernel(DevScene S, int
         }
 
         // ---------------- shading (converged) ----------------
-        if (KF & KF_COUNT) c_rounds += (lane == 0 && __any_sync(FULL, found));
+        if (KF & KF_COUNT) {
+            const bool any_found = __any_sync(FULL, found);   // every lane votes (no short circuit)
+            c_rounds += (lane == 0 && any_found) ? 1 : 0;
+        }
         if (found) {
             last_cell = fcell;
             const int kind = shade_sample<KF>(S, Qx, Qy, Qz, st, bslot, bblk);
