@@ -450,22 +450,30 @@ __global__ void __launch_bounds__(kMarchThreads, 4) march_kernel(DevScene S, int
             // skip target of P:308 (identical result to probing coarse -> fine throughout)
             int e = -1;
             if (!occ_bit(occ_f, fx, fy, fz, Nf)) {
+                // coarsest empty level (default: the finest, known empty) ...
+                int sh = sf, cx = fx, cy = fy, cz = fz;
+                bool chosen = false;
 #pragma unroll
-                for (int lev = 0; lev < MERF_MAX_LEVELS; lev++) {
-                    if (lev < nl && e < 0) {
+                for (int lev = 0; lev < MERF_MAX_LEVELS - 1; lev++) {
+                    if (lev < nl - 1 && !chosen) {
                         const int N = S.level_res[lev];
-                        const int sh = S.level_shift[lev];
-                        const int cx = occ_cell(Qx, sh, N), cy = occ_cell(Qy, sh, N), cz = occ_cell(Qz, sh, N);
-                        if (lev == nl - 1 || !occ_bit(S.occ[lev], cx, cy, cz, N)) {
-                            // jump to the first lattice sample outside this empty cell (ray-AABB exit)
-                            const int K = qa.w;
-                            e = K;
-                            e = min(e, exit_axis(qa.x, uu.x, (cx << sh) - kTwoI, ((cx + 1) << sh) - kTwoI, K));
-                            e = min(e, exit_axis(qa.y, uu.y, (cy << sh) - kTwoI, ((cy + 1) << sh) - kTwoI, K));
-                            e = min(e, exit_axis(qa.z, uu.z, (cz << sh) - kTwoI, ((cz + 1) << sh) - kTwoI, K));
+                        const int shl = S.level_shift[lev];
+                        const int x = occ_cell(Qx, shl, N), y = occ_cell(Qy, shl, N), z = occ_cell(Qz, shl, N);
+                        if (!occ_bit(S.occ[lev], x, y, z, N)) {
+                            sh = shl;
+                            cx = x;
+                            cy = y;
+                            cz = z;
+                            chosen = true;
                         }
                     }
                 }
+                // ... then one convergent exit computation for every skipping lane: jump to the
+                // first lattice sample outside that empty cell (ray-AABB exit)
+                const int K = qa.w;
+                e = min(K, exit_axis(qa.x, uu.x, (cx << sh) - kTwoI, ((cx + 1) << sh) - kTwoI, K));
+                e = min(e, exit_axis(qa.y, uu.y, (cy << sh) - kTwoI, ((cy + 1) << sh) - kTwoI, K));
+                e = min(e, exit_axis(qa.z, uu.z, (cz << sh) - kTwoI, ((cz + 1) << sh) - kTwoI, K));
             }
             if (e >= 0) {
                 k = min(max(k + 1, e), qa.w);
