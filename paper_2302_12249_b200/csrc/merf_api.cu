@@ -22,6 +22,7 @@ using namespace merf;
 struct merf_scene {
     merf_scene_desc desc;
     DevScene dev;
+    MlpParams mlp_params;          // host copy of the MLP weights (shade kernel parameter)
     int device;
     int64_t n_blocks;
     int64_t canonical_blocks;
@@ -215,6 +216,7 @@ extern "C" merf_status merf_scene_upload(const merf_scene_desc* desc, const uint
     UP_TRY(dalloc(s, &d_mlp, kMlpFloats * sizeof(float)));
     UPC_TRY(cudaMemcpyAsync(d_mlp, mlp, kMlpFloats * sizeof(float), cudaMemcpyHostToDevice, cs));
     S.mlp = d_mlp;
+    memcpy(s->mlp_params.w, mlp, sizeof(s->mlp_params.w));
     // ---- planes
     if (use_p) {
         size_t pb = (size_t)3 * desc->R * desc->R * 8;
@@ -427,7 +429,7 @@ static cudaError_t call_march_sph(void* p) {
 }
 static cudaError_t call_shade(void* p) {
     ChunkCall* c = (ChunkCall*)p;
-    return launch_shade(c->kf_shade, c->s->dev, *c->rs, *c->ws, c->out, c->st);
+    return launch_shade(c->kf_shade, c->s->dev, *c->rs, *c->ws, c->out, c->s->mlp_params, c->st);
 }
 
 static merf_status run_chunk(const merf_scene* s, int kf_setup, int kf_march, int kf_shade,

@@ -47,6 +47,13 @@ struct DevScene {
     float step_f, t_min, alpha_skip;
 };
 
+// The deferred MLP's weights as a kernel parameter: every thread reads the same weight at the
+// same time, so they belong in the constant bank (FFMA with a c[][] operand, no load
+// instruction); 3.5 KB of the 32 KB parameter space.
+struct MlpParams {
+    float w[kMlpFloats];
+};
+
 struct CamBatch {
     merf_camera cam[kMaxCams];
     int n;

@@ -635,8 +635,9 @@ __global__ void __launch_bounds__(kSetupThreads) march_sph_kernel(DevScene S, Ra
 // ====================================================================================
 // 3. deferred MLP + store
 // ====================================================================================
-__device__ __forceinline__ void deferred_mlp(const float* __restrict__ w, const float x7[7],
-                                             const float d[3], float out[3]) {
+__device__ __forceinline__ void deferred_mlp(const MlpParams& mp, const float x7[7], const float d[3],
+                                             float out[3]) {
+    const float* w = mp.w;
     float x[34];
 #pragma unroll
     for (int i = 0; i < 7; i++) x[i] = x7[i];
@@ -688,10 +689,7 @@ __device__ __forceinline__ void deferred_mlp(const float* __restrict__ w, const 
 
 template <int KF>
 __global__ void __launch_bounds__(kSetupThreads) shade_kernel(DevScene S, RaySource rs, Workspace ws,
-                                                              void* out) {
-    __shared__ float s_mlp[kMlpFloats];
-    for (int i = threadIdx.x; i < kMlpFloats; i += blockDim.x) s_mlp[i] = S.mlp[i];
-    __syncthreads();
+                                                              void* out, const __grid_constant__ MlpParams mlp) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= rs.n) return;
     const int64_t ray = rs.ray0 + r;
@@ -713,7 +711,7 @@ __global__ void __launch_bounds__(kSetupThreads) shade_kernel(DevScene S, RaySou
     const float4 a0 = ws.accum[r * 2], a1 = ws.accum[r * 2 + 1];
     const float x7[7] = {a0.x, a0.y, a0.z, a1.x, a1.y, a1.z, a1.w};
     float h[3];
-    deferred_mlp(s_mlp, x7, d, h);
+    deferred_mlp(mlp, x7, d, h);
     const float c0 = __saturatef(a0.x + h[0]), c1 = __saturatef(a0.y + h[1]), c2 = __saturatef(a0.z + h[2]);
     auto put = [&](int64_t idx) {
         if (KF & KF_U8) {

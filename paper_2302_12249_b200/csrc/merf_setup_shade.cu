@@ -27,19 +27,19 @@ cudaError_t launch_setup(int kf, const DevScene& S, const RaySource& rs, const W
 
 template <int KF>
 static cudaError_t shade_v(const DevScene& S, const RaySource& rs, const Workspace& ws, void* out,
-                           cudaStream_t st) {
+                           const MlpParams& mlp, cudaStream_t st) {
     if (rs.n <= 0) return cudaSuccess;
     dim3 grid((unsigned)((rs.n + kSetupThreads - 1) / kSetupThreads));
-    shade_kernel<KF><<<grid, kSetupThreads, 0, st>>>(S, rs, ws, out);
+    shade_kernel<KF><<<grid, kSetupThreads, 0, st>>>(S, rs, ws, out, mlp);
     return cudaGetLastError();
 }
 
 cudaError_t launch_shade(int kf, const DevScene& S, const RaySource& rs, const Workspace& ws, void* out,
-                         cudaStream_t st) {
+                         const MlpParams& mlp, cudaStream_t st) {
     switch (kf & (KF_RAYS | KF_U8)) {
-        case 0: return shade_v<0>(S, rs, ws, out, st);
-        case KF_U8: return shade_v<KF_U8>(S, rs, ws, out, st);
-        case KF_RAYS: return shade_v<KF_RAYS>(S, rs, ws, out, st);
+        case 0: return shade_v<0>(S, rs, ws, out, mlp, st);
+        case KF_U8: return shade_v<KF_U8>(S, rs, ws, out, mlp, st);
+        case KF_RAYS: return shade_v<KF_RAYS>(S, rs, ws, out, mlp, st);
         default: return cudaErrorInvalidValue;
     }
 }
