@@ -130,6 +130,7 @@ __device__ __forceinline__ void emit_segment(const DevScene& S, int g, const dou
 template <int KF>
 __global__ void __launch_bounds__(kSetupThreads) setup_kernel(DevScene S, RaySource rs, Workspace ws,
                                                               TraceArgs ta, unsigned long long* stats) {
+    __shared__ double s_cand[kSetupThreads][13];   // 13: odd stride, conflict-free rows
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // index within chunk
     const int64_t ray = rs.ray0 + r;
     bool valid = r < rs.n;
@@ -156,17 +157,17 @@ __global__ void __launch_bounds__(kSetupThreads) setup_kernel(DevScene S, RaySou
         if (valid) {
             double cand[12];
             boundary_candidates(o, d, t_near, cand);
-            // Walk the sorted boundaries (a register shift queue: constant indices only) and
-            // merge equal-region intervals into segments.
-            double b = t_near, seg_start = t_near;
-            int g_cur = -1;
-            for (int it = 0; it < 13; it++) {
-                for (int pop = 0; pop < 12 && cand[0] <= b; pop++) {
+            // Walk the sorted boundaries (staged in this thread's shared-memory row: dynamic
+            // indexing without local memory or register shifting) and merge equal-region
+            // intervals into segments.
+            double* sc = s_cand[threadIdx.x];
 #pragma unroll
-                    for (int q = 0; q < 11; q++) cand[q] = cand[q + 1];
-                    cand[11] = __longlong_as_double(0x7ff0000000000000ll);
-                }
-                const double nb = cand[0];
+            for (int q = 0; q < 12; q++) sc[q] = cand[q];
+            double b = t_near, seg_start = t_near;
+            int g_cur = -1, ci = 0;
+            for (int it = 0; it < 13; it++) {
+                while (ci < 12 && sc[ci] <= b) ci++;
+                const double nb = ci < 12 ? sc[ci] : __longlong_as_double(0x7ff0000000000000ll);
                 const bool last = isinf(nb);
                 const double p = last ? add_rn(mul_rn(b, 2.0), 1.0) : mul_rn(add_rn(b, nb), 0.5);
                 double x[3];
