@@ -140,6 +140,7 @@ static void fill_dev(merf_scene* s) {
     S.n_src = S.use_v + S.use_p[0] + S.use_p[1] + S.use_p[2];
     S.step = d.step;
     S.lattice_step = d.step * (double)kOne;
+    S.inv_step = 1.0 / d.step;
     S.step_f = (float)d.step;
     S.t_min = d.t_min;
     S.alpha_skip = d.alpha_skip;
@@ -802,6 +803,7 @@ extern "C" merf_status merf_qat_step(const merf_qat_desc* d, const float* theta_
     DevScene S{};
     S.step = d->step;
     S.lattice_step = std::ldexp(d->step, kF);
+    S.inv_step = 1.0 / d->step;
     cudaStream_t st = (cudaStream_t)stream;
     {
         int dev = 0;

@@ -44,6 +44,7 @@ struct DevScene {
     int use_v, use_p[3];
     double step;                  // Delta (power of two)
     double lattice_step;          // Delta * 2^F (exact)
+    double inv_step;              // 1 / Delta (exact: Delta is a power of two, validated)
     float step_f, t_min, alpha_skip;
 };
 
@@ -208,7 +209,7 @@ __device__ __forceinline__ bool make_segment(const DevScene& S, int g, const dou
         seg.Qa[q] = (int)__double2ll_rn(mul_rn(ca[q], (double)kOne));
         seg.U[q] = (int)__double2ll_rn(mul_rn(u, S.lattice_step));
     }
-    seg.K = (int)ceil(div_rn(len, S.step));
+    seg.K = (int)ceil(mul_rn(len, S.inv_step));   // == len / Delta exactly (power of two)
     seg.region = g;
     return true;
 }
