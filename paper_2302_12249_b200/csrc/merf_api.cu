@@ -811,7 +811,7 @@ extern "C" merf_status merf_qat_step(const merf_qat_desc* d, const float* theta_
         keep_pool_cached(dev);
     }
     const int64_t nv = (int64_t)d->L * d->L * d->L * 8, np = (int64_t)3 * d->R * d->R * 8;
-    const size_t samp_b = align256((size_t)rs.n * d->max_samples * 48);
+    const size_t samp_b = align256((size_t)rs.n * d->max_samples * 48 + (size_t)rs.n * 64);   // + per-ray rows
     const size_t grid_b = align256((size_t)(nv + np) * 4);
     void* base = nullptr;
     Workspace ws;
@@ -823,6 +823,7 @@ extern "C" merf_status merf_qat_step(const merf_qat_desc* d, const float* theta_
         return fail(MERF_ENOMEM, "QAT scratch allocation failed");
     }
     float* samp = (float*)scratch;
+    float* rayb = samp + (size_t)rs.n * d->max_samples * 12;
     float* vv = (float*)(scratch + samp_b);
     float* vp = vv + nv;
     float* gvv = (float*)(scratch + samp_b + grid_b);
@@ -835,7 +836,7 @@ extern "C" merf_status merf_qat_step(const merf_qat_desc* d, const float* theta_
     if (ce == cudaSuccess) ce = launch_setup(0, S, rs, ws, ta, nullptr, st);
     if (ce == cudaSuccess)
         ce = launch_qat(S, rs, ws, theta_v, theta_p, vv, vp, d->quantize ? 1 : 0, target, rgb_out, gvv, gvp,
-                        grad_v, grad_p, samp, d->max_samples, mlp, loss, ovf,
+                        grad_v, grad_p, samp, d->max_samples, rayb, mlp, loss, ovf,
                         (unsigned long long*)n_samples, d->L, d->R, d->occ_res, occ,
                         (float)d->m_density, (float)d->m_appearance, st);
     cudaFreeAsync(scratch, st);

@@ -47,7 +47,8 @@ struct Workspace;
 cudaError_t launch_qat(const DevScene& S, const RaySource& rs, const Workspace& ws, const float* theta_v,
                        const float* theta_p, float* vv, float* vp, int quant, const float* target, float* rgb,
                        float* gvals_v, float* gvals_p, float* grad_v, float* grad_p, float* samp, int smax,
-                       const float* mlp, double* loss, unsigned int* overflow, unsigned long long* n_samples, int L,
-                       int R, int Nf, const uint32_t* occf, float md, float ma, cudaStream_t st);
+                       float* rayb, const float* mlp, double* loss, unsigned int* overflow,
+                       unsigned long long* n_samples, int L, int R, int Nf, const uint32_t* occf, float md, float ma,
+                       cudaStream_t st);
 
 }  // namespace merf

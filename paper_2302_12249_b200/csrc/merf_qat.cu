@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include "merf_render_kernel.cuh"
+#include "merf_kernels.h"
 
 namespace merf {
 
@@ -96,14 +97,17 @@ __global__ void ste_kernel(const float* __restrict__ theta, const float* __restr
     gtheta[i] = gvals[i] * 2.f * m * s * (1.f - s);
 }
 
-__global__ void __launch_bounds__(128) qat_ray_kernel(DevScene S, RaySource rs, Workspace ws, QatArgs A) {
+// per-ray scratch row (16 floats): [0..6] C_d, F accumulated; [7] sample count (int bits);
+// [8] overflow flag; [9..15] G = dL/d(C_d, F)
+constexpr int kRayRow = 16;
+
+// 2a. forward: composite every occupied lattice sample, storing the per-sample records
+__global__ void __launch_bounds__(128) qat_fwd_kernel(RaySource rs, Workspace ws, QatArgs A, float* rayb) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= rs.n) return;
     int view, px, py;
     if (!ray_pixel(rs, r, view, px, py)) return;
-    const int64_t pix = ((int64_t)view * rs.H + py) * rs.W + px;
     float* rec0 = A.samp + (size_t)r * A.smax * 12;
-    // ---------------- forward ----------------
     float acc[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     float T = 1.f;
     int n = 0;
@@ -138,14 +142,10 @@ __global__ void __launch_bounds__(128) qat_ray_kernel(DevScene S, RaySource rs, 
                 acc[c] = fmaf(alpha * T, xs[c], acc[c]);
             }
             if (n < A.smax) {
-                float* rec = rec0 + (size_t)n * 12;
-                rec[0] = __int_as_float(Qx);
-                rec[1] = __int_as_float(Qy);
-                rec[2] = __int_as_float(Qz);
-                rec[3] = t[0];
-                rec[4] = T;
-#pragma unroll
-                for (int c = 0; c < 7; c++) rec[5 + c] = xs[c];
+                float4* rec = reinterpret_cast<float4*>(rec0 + (size_t)n * 12);
+                rec[0] = make_float4(__int_as_float(Qx), __int_as_float(Qy), __int_as_float(Qz), t[0]);
+                rec[1] = make_float4(T, xs[0], xs[1], xs[2]);
+                rec[2] = make_float4(xs[3], xs[4], xs[5], xs[6]);
             } else {
                 over = true;
             }
@@ -155,12 +155,26 @@ __global__ void __launch_bounds__(128) qat_ray_kernel(DevScene S, RaySource rs, 
     }
     if (over) atomicAdd(A.overflow, 1u);
     if (A.n_samples) atomicAdd(A.n_samples, (unsigned long long)n);
-    // ---------------- deferred MLP forward (Eq. 3) ----------------
+    float* row = rayb + r * kRayRow;
+#pragma unroll
+    for (int c = 0; c < 7; c++) row[c] = acc[c];
+    row[7] = __int_as_float(n);
+    row[8] = over ? 1.f : 0.f;
+}
+
+// 2b. deferred MLP (Eq. 3) forward + backward per ray: colour, loss, G = dL/d(C_d, F)
+__global__ void __launch_bounds__(128) qat_mlp_kernel(RaySource rs, QatArgs A, float* rayb) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= rs.n) return;
+    int view, px, py;
+    if (!ray_pixel(rs, r, view, px, py)) return;
+    const int64_t pix = ((int64_t)view * rs.H + py) * rs.W + px;
+    float* row = rayb + r * kRayRow;
     double od[3], dd[3];
     raygen(rs.cb.cam[view], px, py, od, dd);
     float x[34];
 #pragma unroll
-    for (int c = 0; c < 7; c++) x[c] = acc[c];
+    for (int c = 0; c < 7; c++) x[c] = row[c];
 #pragma unroll
     for (int q = 0; q < 3; q++) x[7 + q] = (float)dd[q];
     int m = 10;
@@ -179,26 +193,32 @@ __global__ void __launch_bounds__(128) qat_ray_kernel(DevScene S, RaySource rs, 
     const float* W2 = A.mlp + 832;
     const float* b2 = A.mlp + 880;
     float h0[16], h1[16], h[3];
+#pragma unroll
     for (int o = 0; o < 16; o++) {
-        float s = b0[o];
-        for (int i = 0; i < 34; i++) s = fmaf(W0[o * 34 + i], x[i], s);
+        float s = __ldg(b0 + o);
+#pragma unroll
+        for (int i = 0; i < 34; i++) s = fmaf(__ldg(W0 + o * 34 + i), x[i], s);
         h0[o] = fmaxf(s, 0.f);
     }
+#pragma unroll
     for (int o = 0; o < 16; o++) {
-        float s = b1[o];
-        for (int i = 0; i < 16; i++) s = fmaf(W1[o * 16 + i], h0[i], s);
+        float s = __ldg(b1 + o);
+#pragma unroll
+        for (int i = 0; i < 16; i++) s = fmaf(__ldg(W1 + o * 16 + i), h0[i], s);
         h1[o] = fmaxf(s, 0.f);
     }
+#pragma unroll
     for (int o = 0; o < 3; o++) {
-        float s = b2[o];
-        for (int i = 0; i < 16; i++) s = fmaf(W2[o * 16 + i], h1[i], s);
+        float s = __ldg(b2 + o);
+#pragma unroll
+        for (int i = 0; i < 16; i++) s = fmaf(__ldg(W2 + o * 16 + i), h1[i], s);
         h[o] = 1.f / (1.f + expf(-s));
     }
     float dC[3];
     double lsum = 0.0;
 #pragma unroll
     for (int c = 0; c < 3; c++) {
-        const float raw = acc[c] + h[c];
+        const float raw = x[c] + h[c];
         const float C = fminf(fmaxf(raw, 0.f), 1.f);
         A.rgb[pix * 3 + c] = C;
         const float e = C - A.target[pix * 3 + c];
@@ -206,57 +226,75 @@ __global__ void __launch_bounds__(128) qat_ray_kernel(DevScene S, RaySource rs, 
         dC[c] = (raw > 0.f && raw < 1.f) ? 2.f * e : 0.f;
     }
     atomicAdd(A.loss, lsum);
-    // ---------------- MLP backward -> G = dL/d(C_d, F) ----------------
     float dz2[3], dh1[16], dh0[16];
 #pragma unroll
     for (int o = 0; o < 3; o++) dz2[o] = dC[o] * h[o] * (1.f - h[o]);
+#pragma unroll
     for (int i = 0; i < 16; i++) {
         float s = 0.f;
-        for (int o = 0; o < 3; o++) s = fmaf(W2[o * 16 + i], dz2[o], s);
+#pragma unroll
+        for (int o = 0; o < 3; o++) s = fmaf(__ldg(W2 + o * 16 + i), dz2[o], s);
         dh1[i] = h1[i] > 0.f ? s : 0.f;
     }
+#pragma unroll
     for (int i = 0; i < 16; i++) {
         float s = 0.f;
-        for (int o = 0; o < 16; o++) s = fmaf(W1[o * 16 + i], dh1[o], s);
+#pragma unroll
+        for (int o = 0; o < 16; o++) s = fmaf(__ldg(W1 + o * 16 + i), dh1[o], s);
         dh0[i] = h0[i] > 0.f ? s : 0.f;
     }
-    float G[7];
+#pragma unroll
     for (int i = 0; i < 7; i++) {
         float s = (i < 3) ? dC[i] : 0.f;
-        for (int o = 0; o < 16; o++) s = fmaf(W0[o * 34 + i], dh0[o], s);
-        G[i] = s;
+#pragma unroll
+        for (int o = 0; o < 16; o++) s = fmaf(__ldg(W0 + o * 34 + i), dh0[o], s);
+        row[9 + i] = s;
     }
-    if (over) return;
-    // ---------------- reverse compositing pass + scatter ----------------
+}
+
+// 2c. reverse compositing pass + scatter of dL/dv to the grid corners
+__global__ void __launch_bounds__(128) qat_bwd_kernel(RaySource rs, QatArgs A, const float* rayb) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= rs.n) return;
+    int view, px, py;
+    if (!ray_pixel(rs, r, view, px, py)) return;
+    const float* row = rayb + r * kRayRow;
+    if (row[8] != 0.f) return;                     // overflowed: gradient dropped (documented)
+    const int n = __float_as_int(row[7]);
+    float G[7];
+#pragma unroll
+    for (int c = 0; c < 7; c++) G[c] = row[9 + c];
+    const float* rec0 = A.samp + (size_t)r * A.smax * 12;
     float Rt[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     for (int i = n - 1; i >= 0; i--) {
-        const float* rec = rec0 + (size_t)i * 12;
-        const float tau = expf(rec[3]);
+        const float4* rec4 = reinterpret_cast<const float4*>(rec0 + (size_t)i * 12);
+        const float4 r0 = rec4[0], r1 = rec4[1], r2 = rec4[2];
+        const float xs[7] = {r1.y, r1.z, r1.w, r2.x, r2.y, r2.z, r2.w};
+        const float tau = expf(r0.w);
         const float alpha = 1.f - expf(-tau * A.step);
-        const float Ti = rec[4];
+        const float Ti = r1.x;
         float gx = 0.f, gr = 0.f;
 #pragma unroll
         for (int c = 0; c < 7; c++) {
-            gx = fmaf(G[c], rec[5 + c], gx);
+            gx = fmaf(G[c], xs[c], gx);
             gr = fmaf(G[c], Rt[c], gr);
         }
         const float dalpha = Ti * (gx - gr);
 #pragma unroll
-        for (int c = 0; c < 7; c++) Rt[c] = fmaf(alpha, rec[5 + c] - Rt[c], Rt[c]);   // a x + (1-a) R
+        for (int c = 0; c < 7; c++) Rt[c] = fmaf(alpha, xs[c] - Rt[c], Rt[c]);   // a x + (1-a) R
         float dt[8];
         dt[0] = dalpha * A.step * (1.f - alpha) * tau;
         const float w = alpha * Ti;
 #pragma unroll
-        for (int c = 0; c < 7; c++) dt[1 + c] = w * G[c] * rec[5 + c] * (1.f - rec[5 + c]);
-        for_corners(A, __float_as_int(rec[0]), __float_as_int(rec[1]), __float_as_int(rec[2]),
-                    [&](int g, int e, float wc) {
-                        if (wc == 0.f) return;
-                        float4* dst = reinterpret_cast<float4*>(
-                            (g == 0) ? A.gv + (size_t)e * 8 : A.gp + ((size_t)(g - 1) * A.R * A.R + e) * 8);
-                        // vector reductions (sm_90+): 2 per corner instead of 8 scalar atomics
-                        atomicAdd(dst, make_float4(wc * dt[0], wc * dt[1], wc * dt[2], wc * dt[3]));
-                        atomicAdd(dst + 1, make_float4(wc * dt[4], wc * dt[5], wc * dt[6], wc * dt[7]));
-                    });
+        for (int c = 0; c < 7; c++) dt[1 + c] = w * G[c] * xs[c] * (1.f - xs[c]);
+        for_corners(A, __float_as_int(r0.x), __float_as_int(r0.y), __float_as_int(r0.z), [&](int g, int e, float wc) {
+            if (wc == 0.f) return;
+            float4* dst = reinterpret_cast<float4*>(
+                (g == 0) ? A.gv + (size_t)e * 8 : A.gp + ((size_t)(g - 1) * A.R * A.R + e) * 8);
+            // vector reductions (sm_90+): 2 per corner instead of 8 scalar atomics
+            atomicAdd(dst, make_float4(wc * dt[0], wc * dt[1], wc * dt[2], wc * dt[3]));
+            atomicAdd(dst + 1, make_float4(wc * dt[4], wc * dt[5], wc * dt[6], wc * dt[7]));
+        });
     }
 }
 
@@ -265,8 +303,9 @@ static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / 
 cudaError_t launch_qat(const DevScene& S, const RaySource& rs, const Workspace& ws, const float* theta_v,
                        const float* theta_p, float* vv, float* vp, int quant, const float* target, float* rgb,
                        float* gvals_v, float* gvals_p, float* grad_v, float* grad_p, float* samp, int smax,
-                       const float* mlp, double* loss, unsigned int* overflow, unsigned long long* n_samples, int L,
-                       int R, int Nf, const uint32_t* occf, float md, float ma, cudaStream_t st) {
+                       float* rayb, const float* mlp, double* loss, unsigned int* overflow,
+                       unsigned long long* n_samples, int L, int R, int Nf, const uint32_t* occf, float md, float ma,
+                       cudaStream_t st) {
     const int64_t nv = (int64_t)L * L * L * 8, np = (int64_t)3 * R * R * 8;
     prequant_kernel<<<nblk(nv, 256), 256, 0, st>>>(theta_v, nv, quant, md, ma, vv);
     prequant_kernel<<<nblk(np, 256), 256, 0, st>>>(theta_p, np, quant, md, ma, vp);
@@ -274,7 +313,9 @@ cudaError_t launch_qat(const DevScene& S, const RaySource& rs, const Workspace& 
     cudaMemsetAsync(gvals_p, 0, np * 4, st);
     QatArgs A{vv, vp, target, rgb, gvals_v, gvals_p, samp, mlp, loss, overflow, n_samples, L, R, smax, Nf,
               kF + 2 - (31 - __builtin_clz((unsigned)Nf)), occf, (float)S.step};
-    qat_ray_kernel<<<nblk(rs.n, 128), 128, 0, st>>>(S, rs, ws, A);
+    qat_fwd_kernel<<<nblk(rs.n, 128), 128, 0, st>>>(rs, ws, A, rayb);
+    qat_mlp_kernel<<<nblk(rs.n, 128), 128, 0, st>>>(rs, A, rayb);
+    qat_bwd_kernel<<<nblk(rs.n, 128), 128, 0, st>>>(rs, A, rayb);
     ste_kernel<<<nblk(nv, 256), 256, 0, st>>>(theta_v, gvals_v, nv, md, ma, grad_v);
     ste_kernel<<<nblk(np, 256), 256, 0, st>>>(theta_p, gvals_p, np, md, ma, grad_p);
     return cudaGetLastError();

@@ -189,7 +189,8 @@ def test_gpu_qat_overflow_drops_only_gradients(M):
     l_full, rgb_full, gv_full, _, o_full = _gpu(M, *case, W_, H_, True)
     l_cut, rgb_cut, gv_cut, _, o_cut = _gpu(M, *case, W_, H_, True, max_samples=4)
     assert o_full == 0 and o_cut > 0
-    assert np.array_equal(rgb_full, rgb_cut) and l_full == l_cut
+    # images identical; the loss is a sum of fp64 atomics (order-dependent at 1 ulp)
+    assert np.array_equal(rgb_full, rgb_cut) and abs(l_full - l_cut) <= 1e-12 * abs(l_full)
     assert np.abs(gv_cut).sum() < np.abs(gv_full).sum()
 
 
