@@ -120,6 +120,8 @@ static void fill_dev(merf_scene* s) {
         S.level_res[i] = i < d.n_levels ? d.level_res[i] : 1;
         S.level_shift[i] = kF + 2 - ilog2i(S.level_res[i]);
     }
+    S.n_fin = S.level_res[S.n_levels - 1];
+    S.s_fin = S.level_shift[S.n_levels - 1];
     S.sV = S.L ? kF + 2 - ilog2i(S.L) : 0;
     S.sP = S.R ? kF + 2 - ilog2i(S.R) : 0;
     S.kd = (float)(2.0 * d.m_density / 255.0);
@@ -241,6 +243,7 @@ extern "C" merf_status merf_scene_upload(const merf_scene_desc* desc, const uint
     for (int i = nl - 2; i >= 0; i--)       // each level from the next finer one (nested)
         UPC_TRY(launch_maxpool_bits(d_occ[i + 1], desc->level_res[i + 1], d_occ[i], desc->level_res[i], cs));
     for (int i = 0; i < MERF_MAX_LEVELS; i++) S.occ[i] = d_occ[i < nl ? i : nl - 1];
+    S.occ_fin = d_occ[nl - 1];
     // ---- block index (K1) + atlas
     if (use_v) {
         const int64_t slots = (int64_t)(desc->L / 8) * (desc->L / 8) * (desc->L / 8);

@@ -30,6 +30,8 @@ struct DevScene {
     const uint32_t* pdens;        // [3][R][R] density quads, byte du + 2 dv
     const uint2* vdens;           // [n_blocks][8][8][8] density octets, byte dx + 2 dy + 4 dz
     const uint32_t* occ[MERF_MAX_LEVELS];
+    const uint32_t* occ_fin;      // = occ[n_levels - 1] (static offset: no dynamic param indexing)
+    int n_fin, s_fin;             // = level_res / level_shift of the finest level
     const float* mlp;             // [883]
     int L, R, nb, n_levels;
     int level_res[MERF_MAX_LEVELS];

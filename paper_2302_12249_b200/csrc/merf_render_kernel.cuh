@@ -359,9 +359,9 @@ __global__ void __launch_bounds__(kMarchThreads, 4) march_kernel(DevScene S, int
     const int lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
     const int nl = S.n_levels;
-    const int Nf = S.level_res[nl - 1];
-    const int sf = S.level_shift[nl - 1];
-    const uint32_t* occ_f = S.occ[nl - 1];
+    const int Nf = S.n_fin;
+    const int sf = S.s_fin;
+    const uint32_t* occ_f = S.occ_fin;
     const bool early_term = !(rflags & MERF_NO_EARLY_TERM);
 
     // per-lane ray state
@@ -586,8 +586,8 @@ __global__ void __launch_bounds__(kSetupThreads) march_sph_kernel(DevScene S, Ra
     int bslot = -1, bblk = -1;
     if (valid) {
         const int nl = S.n_levels;
-        const int Nf = S.level_res[nl - 1];
-        const int sf = S.level_shift[nl - 1];
+        const int Nf = S.n_fin;
+        const int sf = S.s_fin;
         const double stop = sub_rn(2.0, S.step);
         const int kmax = (int)(8.0 / S.step) + 8;
         for (int k = 0; k < kmax; k++) {
@@ -600,7 +600,7 @@ __global__ void __launch_bounds__(kSetupThreads) march_sph_kernel(DevScene S, Ra
             const int Qy = (int)__double2ll_rn(mul_rn(c[1], (double)kOne));
             const int Qz = (int)__double2ll_rn(mul_rn(c[2], (double)kOne));
             const int fx = occ_cell(Qx, sf, Nf), fy = occ_cell(Qy, sf, Nf), fz = occ_cell(Qz, sf, Nf);
-            if (occ_bit(S.occ[nl - 1], fx, fy, fz, Nf)) {
+            if (occ_bit(S.occ_fin, fx, fy, fz, Nf)) {
                 const int kind = shade_sample<KF>(S, Qx, Qy, Qz, st, bslot, bblk);
                 c_donly += kind == 1;
                 c_miss += kind == 2;
