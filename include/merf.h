@@ -110,6 +110,7 @@ typedef struct {
     int64_t region_segments[7]; /* kept segments per region (core, +x, -x, +y, -y, +z, -z)   */
     int64_t march_rounds;       /* warp shading rounds of the persistent march (perf counter) */
     int64_t march_steps;        /* warp traversal iterations (perf counter)                   */
+    int64_t march_lane_rounds;  /* sum over rounds of lanes holding a ray (perf counter)      */
 } merf_stats;
 
 typedef struct {

@@ -363,6 +363,7 @@ static void to_stats(const unsigned long long* h, merf_stats* st) {
     for (int g = 0; g < 7; g++) st->region_segments[g] = (int64_t)h[6 + g];
     st->march_rounds = (int64_t)h[13];
     st->march_steps = (int64_t)h[14];
+    st->march_lane_rounds = (int64_t)h[15];
 }
 
 // ------------------------------------------------------------------------------------

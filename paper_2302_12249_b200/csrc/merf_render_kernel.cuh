@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(kMarchThreads, 4) march_kernel(DevScene S, int
     st.T = 1.f;
     st.cd[0] = st.cd[1] = st.cd[2] = 0.f;
     st.F[0] = st.F[1] = st.F[2] = st.F[3] = 0.f;
-    int c_eval = 0, c_donly = 0, c_skip = 0, c_miss = 0, c_rounds = 0, c_steps = 0;
+    int c_eval = 0, c_donly = 0, c_skip = 0, c_miss = 0, c_rounds = 0, c_steps = 0, c_lanes = 0;
 
     auto finish = [&]() {
         float4* a = ws.accum + (int64_t)ray * 2;
@@ -488,6 +488,7 @@ __global__ void __launch_bounds__(kMarchThreads, 4) march_kernel(DevScene S, int
         if (KF & KF_COUNT) {
             const bool any_found = __any_sync(FULL, found);   // every lane votes (no short circuit)
             c_rounds += (lane == 0 && any_found) ? 1 : 0;
+            c_lanes += (lane == 0) ? __popc(act) : 0;         // lanes holding a ray this round
         }
         if (found) {
             last_cell = fcell;
@@ -516,6 +517,7 @@ __global__ void __launch_bounds__(kMarchThreads, 4) march_kernel(DevScene S, int
         add_stat(stats, 5, c_miss);
         add_stat(stats, 13, c_rounds);
         add_stat(stats, 14, c_steps);
+        add_stat(stats, 15, c_lanes);
     }
 }
 

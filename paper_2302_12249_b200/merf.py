@@ -52,7 +52,8 @@ class merf_camera(C.Structure):
 class merf_stats(C.Structure):
     _fields_ = [("rays", C.c_int64), ("segments", C.c_int64), ("evaluated", C.c_int64),
                 ("density_only", C.c_int64), ("skips", C.c_int64), ("missing_blocks", C.c_int64),
-                ("region_segments", C.c_int64 * 7), ("march_rounds", C.c_int64), ("march_steps", C.c_int64)]
+                ("region_segments", C.c_int64 * 7), ("march_rounds", C.c_int64), ("march_steps", C.c_int64),
+                ("march_lane_rounds", C.c_int64)]
 
     def as_dict(self):
         d = {k: int(getattr(self, k)) for k, _ in self._fields_ if k != "region_segments"}
