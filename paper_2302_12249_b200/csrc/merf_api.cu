@@ -65,6 +65,8 @@ merf_status merf_set_error(merf_status s, const char* msg) {   // for the other 
                         "%s: %s (%s:%d)", #expr, cudaGetErrorString(_e), __FILE__, __LINE__); \
     } while (0)
 
+static const int kSkipTabMaxRes = 512;
+
 static bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
 static int ilog2i(int64_t v) { int n = 0; while ((int64_t(1) << n) < v) n++; return n; }
 static int64_t occ_words(int N) { return ((int64_t)N * N * N + 31) / 32; }
@@ -244,6 +246,13 @@ extern "C" merf_status merf_scene_upload(const merf_scene_desc* desc, const uint
         UPC_TRY(launch_maxpool_bits(d_occ[i + 1], desc->level_res[i + 1], d_occ[i], desc->level_res[i], cs));
     for (int i = 0; i < MERF_MAX_LEVELS; i++) S.occ[i] = d_occ[i < nl ? i : nl - 1];
     S.occ_fin = d_occ[nl - 1];
+    S.skiptab = nullptr;
+    if (Nf <= kSkipTabMaxRes && Nf >= 2) {    // 4 bits per finest cell (64 MB at 512^3)
+        uint32_t* d_tab;
+        UP_TRY(dalloc(s, &d_tab, (size_t)Nf * Nf * Nf / 2));
+        UPC_TRY(launch_skiptab(d_occ, desc->level_res, nl, d_tab, cs));
+        S.skiptab = d_tab;
+    }
     // ---- block index (K1) + atlas
     if (use_v) {
         const int64_t slots = (int64_t)(desc->L / 8) * (desc->L / 8) * (desc->L / 8);

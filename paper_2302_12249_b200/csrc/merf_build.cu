@@ -335,4 +335,62 @@ cudaError_t launch_contract(const double* x, int64_t n, double* y, int32_t* regi
     return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------------------------
+// Skip table: for every finest cell, code = level_shift(coarsest empty level) - 16, or 0 if
+// the finest cell is occupied.  The march reads one nibble instead of searching the levels
+// (same skip target as the coarse -> fine search of P:307-308, so traces are unchanged).
+// One thread per 8 cells (one output word).
+// ------------------------------------------------------------------------------------
+struct LevelSet {
+    const uint32_t* occ[MERF_MAX_LEVELS];
+    int res[MERF_MAX_LEVELS];
+    int shift[MERF_MAX_LEVELS];
+    int n;
+};
+
+__global__ void skiptab_kernel(LevelSet ls, uint32_t* __restrict__ tab) {
+    const int nl = ls.n;
+    const int N = ls.res[nl - 1];
+    const int64_t words = (int64_t)N * N * N / 8;
+    const int64_t wi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (wi >= words) return;
+    uint32_t out = 0;
+    for (int q = 0; q < 8; q++) {
+        const int64_t c = wi * 8 + q;
+        const int x = (int)(c % N), y = (int)((c / N) % N), z = (int)(c / ((int64_t)N * N));
+        const int64_t lf = c;
+        uint32_t code = 0;
+        if (!((__ldg(ls.occ[nl - 1] + (lf >> 5)) >> (lf & 31)) & 1u)) {
+            int sh = ls.shift[nl - 1];
+            for (int lev = 0; lev < nl - 1; lev++) {
+                const int f = N / ls.res[lev], M = ls.res[lev];
+                const int64_t l = ((int64_t)(z / f) * M + (y / f)) * M + (x / f);
+                if (!((__ldg(ls.occ[lev] + (l >> 5)) >> (l & 31)) & 1u)) {
+                    sh = ls.shift[lev];
+                    break;
+                }
+            }
+            code = (uint32_t)(sh - 16);
+        }
+        out |= code << (4 * q);
+    }
+    tab[wi] = out;
+}
+
+cudaError_t launch_skiptab(const uint32_t* const* occ, const int* res, int nl, uint32_t* tab, cudaStream_t st) {
+    LevelSet ls{};
+    ls.n = nl;
+    for (int i = 0; i < nl; i++) {
+        ls.occ[i] = occ[i];
+        ls.res[i] = res[i];
+        int m = 0;
+        while ((1 << m) < res[i]) m++;
+        ls.shift[i] = kF + 2 - m;
+    }
+    const int N = res[nl - 1];
+    const int64_t words = (int64_t)N * N * N / 8;
+    skiptab_kernel<<<(unsigned)((words + 255) / 256), 256, 0, st>>>(ls, tab);
+    return cudaGetLastError();
+}
+
 }  // namespace merf

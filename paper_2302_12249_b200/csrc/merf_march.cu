@@ -36,12 +36,31 @@ static cudaError_t march_v(const DevScene& S, int64_t n, const Workspace& ws, ui
     return cudaGetLastError();
 }
 
+// the per-cell skip table is used when the scene has one, unless MERF_NO_SKIPTAB is set (tests
+// and ablations run both traversals)
+static bool use_skiptab(const DevScene& S) {
+    if (!S.skiptab) return false;
+    const char* e = getenv("MERF_NO_SKIPTAB");
+    return !(e && e[0] && e[0] != '0');
+}
+
 cudaError_t launch_march(int kf, const DevScene& S, int64_t n, const Workspace& ws, uint32_t rflags,
                          const TraceArgs& ta, unsigned long long* stats, cudaStream_t st) {
+    const bool tab = use_skiptab(S);
     if (S.n_src == 4 && !(kf & (KF_TRACE | KF_DENSE))) {    // production variants
+        if (tab) {
+            if (kf & KF_COUNT) return march_v<KF_ALLSRC | KF_SKIPTAB | KF_COUNT>(S, n, ws, rflags, ta, stats, st);
+            return march_v<KF_ALLSRC | KF_SKIPTAB>(S, n, ws, rflags, ta, stats, st);
+        }
         if (kf & KF_COUNT) return march_v<KF_ALLSRC | KF_COUNT>(S, n, ws, rflags, ta, stats, st);
         return march_v<KF_ALLSRC>(S, n, ws, rflags, ta, stats, st);
     }
+    if (tab && (kf & (KF_TRACE | KF_DENSE | KF_COUNT)) == KF_TRACE)
+        return march_v<KF_TRACE | KF_SKIPTAB>(S, n, ws, rflags, ta, stats, st);
+    if (tab && (kf & (KF_TRACE | KF_DENSE | KF_COUNT)) == 0)
+        return march_v<KF_SKIPTAB>(S, n, ws, rflags, ta, stats, st);
+    if (tab && (kf & (KF_TRACE | KF_DENSE | KF_COUNT)) == KF_COUNT)
+        return march_v<KF_SKIPTAB | KF_COUNT>(S, n, ws, rflags, ta, stats, st);
     switch (kf & (KF_TRACE | KF_DENSE | KF_COUNT)) {
         case 0: return march_v<0>(S, n, ws, rflags, ta, stats, st);
         case KF_COUNT: return march_v<KF_COUNT>(S, n, ws, rflags, ta, stats, st);

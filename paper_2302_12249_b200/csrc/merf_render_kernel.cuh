@@ -33,6 +33,7 @@ enum : int {
     KF_DENSE = 16,      // dense stepping gated by the finest level (debug)
     KF_SEGS = 32,       // record contracted segments only (no marching)
     KF_ALLSRC = 64,     // all four sources present (compile-time; the production variant)
+    KF_SKIPTAB = 128,   // skip level from the per-cell table (S.skiptab) instead of the level search
 };
 
 constexpr int kSetupThreads = 128;
@@ -450,27 +451,45 @@ __global__ void __launch_bounds__(kMarchThreads, 4) march_kernel(DevScene S, int
             // cell searches coarse -> fine for the coarsest empty level, whose cell exit is the
             // skip target of P:308 (identical result to probing coarse -> fine throughout)
             int e = -1;
-            if (!occ_bit(occ_f, fx, fy, fz, Nf)) {
-                // coarsest empty level (default: the finest, known empty) ...
-                int sh = sf, cx = fx, cy = fy, cz = fz;
-                bool chosen = false;
+            bool skip;
+            int sh = sf, cx = fx, cy = fy, cz = fz;
+            if (KF & KF_SKIPTAB) {
+                // one probe: 0 = occupied, else the shift of the coarsest empty level - 16
+                const unsigned code =
+                    (__ldg(S.skiptab + ((unsigned)fcell >> 3)) >> (((unsigned)fcell & 7u) * 4u)) & 15u;
+                skip = code != 0u;
+                if (skip) {
+                    sh = (int)code + 16;
+                    const int N = 1 << (kF + 2 - sh);
+                    cx = occ_cell(Qx, sh, N);
+                    cy = occ_cell(Qy, sh, N);
+                    cz = occ_cell(Qz, sh, N);
+                }
+            } else {
+                skip = !occ_bit(occ_f, fx, fy, fz, Nf);
+                if (skip) {
+                    // coarsest empty level (default: the finest, known empty)
+                    bool chosen = false;
 #pragma unroll
-                for (int lev = 0; lev < MERF_MAX_LEVELS - 1; lev++) {
-                    if (lev < nl - 1 && !chosen) {
-                        const int N = S.level_res[lev];
-                        const int shl = S.level_shift[lev];
-                        const int x = occ_cell(Qx, shl, N), y = occ_cell(Qy, shl, N), z = occ_cell(Qz, shl, N);
-                        if (!occ_bit(S.occ[lev], x, y, z, N)) {
-                            sh = shl;
-                            cx = x;
-                            cy = y;
-                            cz = z;
-                            chosen = true;
+                    for (int lev = 0; lev < MERF_MAX_LEVELS - 1; lev++) {
+                        if (lev < nl - 1 && !chosen) {
+                            const int N = S.level_res[lev];
+                            const int shl = S.level_shift[lev];
+                            const int x = occ_cell(Qx, shl, N), y = occ_cell(Qy, shl, N), z = occ_cell(Qz, shl, N);
+                            if (!occ_bit(S.occ[lev], x, y, z, N)) {
+                                sh = shl;
+                                cx = x;
+                                cy = y;
+                                cz = z;
+                                chosen = true;
+                            }
                         }
                     }
                 }
-                // ... then one convergent exit computation for every skipping lane: jump to the
-                // first lattice sample outside that empty cell (ray-AABB exit)
+            }
+            if (skip) {
+                // one convergent exit computation for every skipping lane: jump to the first
+                // lattice sample outside that empty cell (ray-AABB exit)
                 const int K = qa.w;
                 e = min(K, exit_axis(qa.x, uu.x, (cx << sh) - kTwoI, ((cx + 1) << sh) - kTwoI, K));
                 e = min(e, exit_axis(qa.y, uu.y, (cy << sh) - kTwoI, ((cy + 1) << sh) - kTwoI, K));

@@ -475,3 +475,32 @@ def test_render_argument_errors(M, c1_scene):
     with pytest.raises(M.MerfError):
         M.merf_render(s.handle, bad_cam, W, H, out)
     s.close()
+
+
+def test_skip_table_equals_level_search(M, c2):
+    """the per-cell skip table (one 4-bit probe) and the coarse -> fine level search give the
+    same skips: identical frames, counters and traces (MERF_NO_SKIPTAB selects the search)."""
+    import os
+    import torch
+    cams, W, H = config_cameras("c2")
+    s = M.Scene(c2)
+    pix = np.random.default_rng(3).integers(0, W * H, 300)
+    outs, stats, traces = [], [], []
+    for env in ("0", "1"):
+        os.environ["MERF_NO_SKIPTAB"] = env
+        try:
+            out, st = s.render(cams, W, H, stats=True)
+            pid = torch.as_tensor(pix, device="cuda")
+            cells = torch.zeros((len(pix), 2048), dtype=torch.int64, device="cuda")
+            cnt = torch.zeros(len(pix), dtype=torch.int32, device="cuda")
+            M.merf_trace(s.handle, cams[0], W, pid, 2048, cells, None, cnt)
+            torch.cuda.synchronize()
+        finally:
+            os.environ.pop("MERF_NO_SKIPTAB", None)
+        outs.append(out.cpu().numpy())
+        stats.append({k: st[k] for k in ("evaluated", "skips", "density_only")})
+        traces.append((cells.cpu().numpy(), cnt.cpu().numpy()))
+    s.close()
+    assert np.array_equal(outs[0], outs[1])
+    assert stats[0] == stats[1]
+    assert np.array_equal(traces[0][0], traces[1][0]) and np.array_equal(traces[0][1], traces[1][1])
