@@ -250,7 +250,7 @@ extern "C" merf_status merf_scene_upload(const merf_scene_desc* desc, const uint
     if (Nf <= kSkipTabMaxRes && Nf >= 2) {    // 4 bits per finest cell (64 MB at 512^3)
         uint32_t* d_tab;
         UP_TRY(dalloc(s, &d_tab, (size_t)Nf * Nf * Nf / 2));
-        UPC_TRY(launch_skiptab(d_occ, desc->level_res, nl, d_tab, cs));
+        UPC_TRY(launch_skiptab(d_occ[nl - 1], Nf, d_tab, cs));
         S.skiptab = d_tab;
     }
     // ---- block index (K1) + atlas

@@ -336,21 +336,22 @@ cudaError_t launch_contract(const double* x, int64_t n, double* y, int32_t* regi
 }
 
 // ------------------------------------------------------------------------------------
-// Skip table: for every finest cell, code = level_shift(coarsest empty level) - 16, or 0 if
-// the finest cell is occupied.  The march reads one nibble instead of searching the levels
-// (same skip target as the coarse -> fine search of P:307-308, so traces are unchanged).
-// One thread per 8 cells (one output word).
+// Skip table: for every finest cell, code = lattice shift of the coarsest EMPTY dyadic cell
+// containing it, minus 16, or 0 if the finest cell is occupied.  The dyadic levels are the
+// OR-pools of the finest level at every power-of-two resolution N_f/2, ..., 1 -- the
+// multi-level occupancy grid of P:307-308 completed to all scales, so each skip leaves the
+// largest aligned empty cell around the sample.  Only empty space is skipped, so the set of
+// evaluated samples (and every trace) is the one of dense stepping.  One thread per 8 cells.
 // ------------------------------------------------------------------------------------
+constexpr int kMaxDyadic = 16;
 struct LevelSet {
-    const uint32_t* occ[MERF_MAX_LEVELS];
-    int res[MERF_MAX_LEVELS];
-    int shift[MERF_MAX_LEVELS];
+    const uint32_t* occ[kMaxDyadic];   // coarse -> fine, res 1, 2, 4, ..., N_f
     int n;
 };
 
 __global__ void skiptab_kernel(LevelSet ls, uint32_t* __restrict__ tab) {
     const int nl = ls.n;
-    const int N = ls.res[nl - 1];
+    const int N = 1 << (nl - 1);
     const int64_t words = (int64_t)N * N * N / 8;
     const int64_t wi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (wi >= words) return;
@@ -358,39 +359,48 @@ __global__ void skiptab_kernel(LevelSet ls, uint32_t* __restrict__ tab) {
     for (int q = 0; q < 8; q++) {
         const int64_t c = wi * 8 + q;
         const int x = (int)(c % N), y = (int)((c / N) % N), z = (int)(c / ((int64_t)N * N));
-        const int64_t lf = c;
         uint32_t code = 0;
-        if (!((__ldg(ls.occ[nl - 1] + (lf >> 5)) >> (lf & 31)) & 1u)) {
-            int sh = ls.shift[nl - 1];
-            for (int lev = 0; lev < nl - 1; lev++) {
-                const int f = N / ls.res[lev], M = ls.res[lev];
-                const int64_t l = ((int64_t)(z / f) * M + (y / f)) * M + (x / f);
-                if (!((__ldg(ls.occ[lev] + (l >> 5)) >> (l & 31)) & 1u)) {
-                    sh = ls.shift[lev];
+        if (!((__ldg(ls.occ[nl - 1] + (c >> 5)) >> (c & 31)) & 1u)) {
+            int lev = nl - 1;                    // the finest (known empty) unless a coarser one is
+            for (int l = 0; l < nl - 1; l++) {
+                const int sft = nl - 1 - l, M = 1 << l;
+                const int64_t li = ((int64_t)(z >> sft) * M + (y >> sft)) * M + (x >> sft);
+                if (!((__ldg(ls.occ[l] + (li >> 5)) >> (li & 31)) & 1u)) {
+                    lev = l;
                     break;
                 }
             }
-            code = (uint32_t)(sh - 16);
+            code = (uint32_t)(kF + 2 - lev - 16);   // lattice shift of resolution 2^lev, - 16
         }
         out |= code << (4 * q);
     }
     tab[wi] = out;
 }
 
-cudaError_t launch_skiptab(const uint32_t* const* occ, const int* res, int nl, uint32_t* tab, cudaStream_t st) {
+cudaError_t launch_skiptab(const uint32_t* finest, int Nf, uint32_t* tab, cudaStream_t st) {
+    int nl = 0;
+    while ((1 << nl) < Nf) nl++;
+    nl += 1;                                   // resolutions 1 .. Nf
+    if (nl > kMaxDyadic) return cudaErrorInvalidValue;
     LevelSet ls{};
     ls.n = nl;
-    for (int i = 0; i < nl; i++) {
-        ls.occ[i] = occ[i];
-        ls.res[i] = res[i];
-        int m = 0;
-        while ((1 << m) < res[i]) m++;
-        ls.shift[i] = kF + 2 - m;
+    ls.occ[nl - 1] = finest;
+    uint32_t* tmp[kMaxDyadic] = {};
+    cudaError_t e = cudaSuccess;
+    for (int l = nl - 2; l >= 0 && e == cudaSuccess; l--) {   // each level from the next finer
+        const int M = 1 << l;
+        e = cudaMallocAsync(&tmp[l], (((size_t)M * M * M + 31) / 32) * 4, st);
+        if (e == cudaSuccess) e = launch_maxpool_bits(ls.occ[l + 1], 2 * M, tmp[l], M, st);
+        ls.occ[l] = tmp[l];
     }
-    const int N = res[nl - 1];
-    const int64_t words = (int64_t)N * N * N / 8;
-    skiptab_kernel<<<(unsigned)((words + 255) / 256), 256, 0, st>>>(ls, tab);
-    return cudaGetLastError();
+    if (e == cudaSuccess) {
+        const int64_t words = (int64_t)Nf * Nf * Nf / 8;
+        skiptab_kernel<<<(unsigned)((words + 255) / 256), 256, 0, st>>>(ls, tab);
+        e = cudaGetLastError();
+    }
+    for (int l = 0; l < kMaxDyadic; l++)
+        if (tmp[l]) cudaFreeAsync(tmp[l], st);
+    return e;
 }
 
 }  // namespace merf

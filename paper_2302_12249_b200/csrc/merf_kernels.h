@@ -38,8 +38,8 @@ cudaError_t launch_bake_occupancy(const double* x, const double* tau, const doub
                                   double tau_thr, double w_thr, int N, uint32_t* bits, cudaStream_t st);
 cudaError_t launch_pack_atlas(const uint8_t* dense, int L, const int32_t* index, int64_t n_blocks,
                               uint8_t* atlas, cudaStream_t st);
-// skip table of the march (one 4-bit code per finest cell; N >= 2, N^3 multiple of 8)
-cudaError_t launch_skiptab(const uint32_t* const* occ, const int* res, int nl, uint32_t* tab, cudaStream_t st);
+// skip table of the march (one 4-bit code per finest cell over all dyadic levels; Nf >= 2)
+cudaError_t launch_skiptab(const uint32_t* finest, int Nf, uint32_t* tab, cudaStream_t st);
 cudaError_t launch_contract(const double* x, int64_t n, double* y, int32_t* region, cudaStream_t st);
 
 // NEXT-3 quantisation-aware forward/backward (merf_qat.cu)

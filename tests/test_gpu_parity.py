@@ -195,7 +195,16 @@ def test_c1_frame_colour(M, c1_scene):
     assert psnr(g, ref["rgb"]) >= MIN_PSNR
     assert st["rays"] == W * H
     assert st["evaluated"] == ref["stats"]["evaluated"]
-    assert st["skips"] == ref["stats"]["skips"]
+    # the default traversal skips with all dyadic levels (reading D23): never more skips than
+    # the scene's own levels; the level search (MERF_NO_SKIPTAB) reproduces the oracle's count
+    assert st["skips"] <= ref["stats"]["skips"]
+    import os
+    os.environ["MERF_NO_SKIPTAB"] = "1"
+    try:
+        _, st_lv = _gpu_frame(M, c1_scene, cams, W, H)
+    finally:
+        os.environ.pop("MERF_NO_SKIPTAB", None)
+    assert st_lv["skips"] == ref["stats"]["skips"] and st_lv["evaluated"] == ref["stats"]["evaluated"]
     assert st["segments"] == ref["stats"]["segments"]
     assert st["missing_blocks"] == 0
 
@@ -478,8 +487,10 @@ def test_render_argument_errors(M, c1_scene):
 
 
 def test_skip_table_equals_level_search(M, c2):
-    """the per-cell skip table (one 4-bit probe) and the coarse -> fine level search give the
-    same skips: identical frames, counters and traces (MERF_NO_SKIPTAB selects the search)."""
+    """the per-cell skip table (one 4-bit probe over all dyadic levels) and the coarse -> fine
+    search over the scene's levels skip only empty space: identical frames, evaluated samples
+    and traces; the table's larger cells need no more skips (MERF_NO_SKIPTAB selects the
+    search)."""
     import os
     import torch
     cams, W, H = config_cameras("c2")
@@ -502,5 +513,7 @@ def test_skip_table_equals_level_search(M, c2):
         traces.append((cells.cpu().numpy(), cnt.cpu().numpy()))
     s.close()
     assert np.array_equal(outs[0], outs[1])
-    assert stats[0] == stats[1]
+    assert stats[0]["evaluated"] == stats[1]["evaluated"]
+    assert stats[0]["density_only"] == stats[1]["density_only"]
+    assert stats[0]["skips"] <= stats[1]["skips"]
     assert np.array_equal(traces[0][0], traces[1][0]) and np.array_equal(traces[0][1], traces[1][1])
