@@ -293,7 +293,7 @@ def main():
                 "avg_launch_ms": avg_launch_ms, "launches": kt["march_launches"],
                 "algorithmic_bytes_per_launch": bytes_per_launch,
                 "bytes_model": "160 B per evaluated sample with alpha > 0, 20 B per density-only "
-                               "sample (SURVEY 8(d)); launch = one chunk of 8 views",
+                               "sample (SURVEY 8(d)); launch = one chunk of 16 views",
                 "pipeline_ms_per_step": {"setup": kt["setup_ms"] / args.steps,
                                          "march": kt["march_ms"] / args.steps,
                                          "shade": kt["shade_ms"] / args.steps,

@@ -24,7 +24,7 @@ def main():
     r = dict(zip(hdr, data[0]))
     rd, wr = float(r["dram__bytes_read.sum"]), float(r["dram__bytes_write.sum"])
     d = {"source": f"{a.report.split('/')[-1]} (ncu --set full --clock-control none, {r['Kernel Name'].split('(')[0]},"
-                   " one launch = 8 views at 1080p, tools/prof_render.py --views 8)",
+                   " one launch = 16 views at 1080p, tools/prof_render.py --views 16)",
          "dram_bytes_read_per_launch": rd, "dram_bytes_write_per_launch": wr, "dram_bytes_per_launch": rd + wr,
          "ncu_duration_ns": float(r["gpu__time_duration.sum"]),
          "note": "includes the workspace (segments read, accumulators written); scene texels hit L1/L2"}
