@@ -225,16 +225,21 @@ extern "C" merf_status merf_scene_upload(const merf_scene_desc* desc, const uint
     // ---- planes
     if (use_p) {
         size_t pb = (size_t)3 * desc->R * desc->R * 8;
-        uint8_t* d_pl;
-        // padded by one texel row: the clamped upper-edge corner (weight 0) stays in bounds
-        UP_TRY(dalloc(s, &d_pl, pb + (size_t)(desc->R + 2) * 8));
-        UPC_TRY(cudaMemsetAsync(d_pl + pb, 0, (size_t)(desc->R + 2) * 8, cs));
+        uint8_t* d_pl;                         // AoS staging, freed once the layouts are built
+        UPC_TRY(cudaMallocAsync((void**)&d_pl, pb, cs));
         UPC_TRY(cudaMemcpyAsync(d_pl, planes, pb, cudaMemcpyHostToDevice, cs));
-        S.planes = d_pl;
+        uint4* d_pp;
+        // padded by one entry row: the clamped upper-edge row (weight 0) stays in bounds
+        const size_t ppb = ((size_t)3 * desc->R * desc->R + desc->R) * 16;
+        UP_TRY(dalloc(s, &d_pp, ppb));
+        UPC_TRY(cudaMemsetAsync(d_pp, 0, ppb, cs));
+        UPC_TRY(launch_pack_pairs(d_pl, desc->R, d_pp, nullptr, 0, nullptr, cs));
+        S.plane_pairs = d_pp;
         uint32_t* d_pd;
         UP_TRY(dalloc(s, &d_pd, (size_t)3 * desc->R * desc->R * 4));
         UPC_TRY(launch_pack_density(d_pl, desc->R, d_pd, nullptr, 0, nullptr, cs));
         S.pdens = d_pd;
+        UPC_TRY(cudaFreeAsync(d_pl, cs));
     }
     // ---- occupancy pyramid (K0)
     const int nl = desc->n_levels;
@@ -297,15 +302,21 @@ extern "C" merf_status merf_scene_upload(const merf_scene_desc* desc, const uint
             return bail(fail(MERF_EMISMATCH, "block index unsound or out of range at %llu slots "
                                              "(an occupied cell's block is missing)", bad));
         size_t ab = (size_t)n_blocks * 729 * 8;
-        uint8_t* d_at;
-        UP_TRY(dalloc(s, &d_at, ab));
-        if (ab) UPC_TRY(cudaMemcpyAsync(d_at, atlas, ab, cudaMemcpyHostToDevice, cs));
+        uint8_t* d_at = nullptr;               // AoS staging, freed once the layouts are built
+        if (ab) {
+            UPC_TRY(cudaMallocAsync((void**)&d_at, ab, cs));
+            UPC_TRY(cudaMemcpyAsync(d_at, atlas, ab, cudaMemcpyHostToDevice, cs));
+        }
         S.block_index = d_idx;
-        S.atlas = d_at;
+        uint4* d_ap;
+        UP_TRY(dalloc(s, &d_ap, (size_t)n_blocks * 648 * 16));
+        if (n_blocks) UPC_TRY(launch_pack_pairs(nullptr, 0, nullptr, d_at, n_blocks, d_ap, cs));
+        S.atlas_pairs = d_ap;
         uint2* d_vd;
         UP_TRY(dalloc(s, &d_vd, (size_t)n_blocks * 512 * 8));
         if (n_blocks) UPC_TRY(launch_pack_density(nullptr, 0, nullptr, d_at, n_blocks, d_vd, cs));
         S.vdens = d_vd;
+        if (d_at) UPC_TRY(cudaFreeAsync(d_at, cs));
     }
     UPC_TRY(cudaStreamSynchronize(cs));
     cudaStreamDestroy(cs);

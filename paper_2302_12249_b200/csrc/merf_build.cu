@@ -403,4 +403,52 @@ cudaError_t launch_skiptab(const uint32_t* finest, int Nf, uint32_t* tab, cudaSt
     return e;
 }
 
+// ------------------------------------------------------------------------------------
+// Appearance pair layouts (see DevScene): word k of entry u = bytes (c_{2k+1}(u),
+// c_{2k+1}(u+1), c_{2k+2}(u), c_{2k+2}(u+1)) with c8 := c0 (density, unused by the pass).
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ uint4 pair_entry(uint2 a, uint2 b) {
+    // a.x = c0 c1 c2 c3, a.y = c4 c5 c6 c7 (texel u); b the same for texel u + 1
+    uint4 o;
+    o.x = __byte_perm(a.x, b.x, 0x6251);                                   // c1 c1' c2 c2'
+    o.y = __byte_perm(__byte_perm(a.x, b.x, 0x0073), __byte_perm(a.y, b.y, 0x0040), 0x5410);   // c3 c3' c4 c4'
+    o.z = __byte_perm(a.y, b.y, 0x6251);                                   // c5 c5' c6 c6'
+    o.w = __byte_perm(__byte_perm(a.y, b.y, 0x0073), __byte_perm(a.x, b.x, 0x0040), 0x5410);   // c7 c7' c0 c0'
+    return o;
+}
+
+__global__ void pack_plane_pairs_kernel(const uint2* __restrict__ planes, int R, uint4* __restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // entry (a, v, u)
+    const int64_t n = (int64_t)3 * R * R;
+    if (i >= n) return;
+    const int u = (int)(i % R);
+    const uint2 a = planes[i];
+    const uint2 b = u + 1 < R ? planes[i + 1] : a;    // u + 1 = R: weight 0 (clamped texel)
+    out[i] = pair_entry(a, b);
+}
+
+__global__ void pack_atlas_pairs_kernel(const uint2* __restrict__ atlas, int64_t n_blocks, uint4* __restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // entry (b, z, y, x < 8)
+    if (i >= n_blocks * 648) return;
+    const int64_t row = i / 8;                                          // (b, z, y)
+    const int x = (int)(i % 8);
+    const uint2* src = atlas + row * 9 + x;
+    out[i] = pair_entry(src[0], src[1]);
+}
+
+cudaError_t launch_pack_pairs(const uint8_t* planes, int R, uint4* plane_pairs, const uint8_t* atlas,
+                              int64_t n_blocks, uint4* atlas_pairs, cudaStream_t st) {
+    if (planes && R > 0) {
+        const int64_t n = (int64_t)3 * R * R;
+        pack_plane_pairs_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+            reinterpret_cast<const uint2*>(planes), R, plane_pairs);
+    }
+    if (atlas && n_blocks > 0) {
+        const int64_t n = n_blocks * 648;
+        pack_atlas_pairs_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+            reinterpret_cast<const uint2*>(atlas), n_blocks, atlas_pairs);
+    }
+    return cudaGetLastError();
+}
+
 }  // namespace merf

@@ -24,9 +24,12 @@ constexpr int kMaxCams = 16;                              // cameras per launch 
 constexpr int kMlpFloats = 883;
 
 struct DevScene {
-    const uint8_t* planes;        // [3][R][R][8]
+    // appearance layouts, pair-interleaved along the fastest axis: entry (.., u) holds texels u
+    // and u+1 as 4 words (c1 c1' c2 c2' | c3 c3' c4 c4' | c5 c5' c6 c6' | c7 c7' c0 c0'), so
+    // one 16-byte load feeds 7 dp2a directly (no byte gathering)
+    const uint4* plane_pairs;     // [3][R][R] (+ one padding row)
     const int32_t* block_index;   // [(L/8)^3]
-    const uint8_t* atlas;         // [n_blocks][9][9][9][8]
+    const uint4* atlas_pairs;     // [n_blocks][9][9][8]
     const uint32_t* pdens;        // [3][R][R] density quads, byte du + 2 dv
     const uint2* vdens;           // [n_blocks][8][8][8] density octets, byte dx + 2 dy + 4 dz
     const uint32_t* occ[MERF_MAX_LEVELS];

@@ -38,6 +38,9 @@ cudaError_t launch_bake_occupancy(const double* x, const double* tau, const doub
                                   double tau_thr, double w_thr, int N, uint32_t* bits, cudaStream_t st);
 cudaError_t launch_pack_atlas(const uint8_t* dense, int L, const int32_t* index, int64_t n_blocks,
                               uint8_t* atlas, cudaStream_t st);
+// appearance pair layouts from the AoS planes / atlas (see DevScene)
+cudaError_t launch_pack_pairs(const uint8_t* planes, int R, uint4* plane_pairs, const uint8_t* atlas,
+                              int64_t n_blocks, uint4* atlas_pairs, cudaStream_t st);
 // skip table of the march (one 4-bit code per finest cell over all dyadic levels; Nf >= 2)
 cudaError_t launch_skiptab(const uint32_t* finest, int Nf, uint32_t* tab, cudaStream_t st);
 cudaError_t launch_contract(const double* x, int64_t n, double* y, int32_t* region, cudaStream_t st);

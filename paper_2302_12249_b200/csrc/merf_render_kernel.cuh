@@ -213,21 +213,17 @@ struct RayState {
 };
 
 
-// Appearance accumulation of a corner PAIR (texels a, b; 16-bit weights packed in wp):
-// integer dot products dp2a over byte pairs gathered with PRMT, 7 channels in 4 PRMT +
-// 7 DP2A (vs 14 byte converts + 14 FMA in fp32).  acc[c] is in units of 1/65535 byte.
-__device__ __forceinline__ void acc_pair(uint32_t acc[7], uint2 a, uint2 b, uint32_t wp) {
-    const uint32_t rg = __byte_perm(a.x, b.x, 0x6251);     // r_a r_b g_a g_b
-    const uint32_t bd = __byte_perm(a.x, b.x, 0x0073);     // b_a b_b
-    const uint32_t f01 = __byte_perm(a.y, b.y, 0x5140);    // f0_a f0_b f1_a f1_b
-    const uint32_t f23 = __byte_perm(a.y, b.y, 0x7362);    // f2_a f2_b f3_a f3_b
-    acc[0] = __dp2a_lo(wp, rg, acc[0]);
-    acc[1] = __dp2a_hi(wp, rg, acc[1]);
-    acc[2] = __dp2a_lo(wp, bd, acc[2]);
-    acc[3] = __dp2a_lo(wp, f01, acc[3]);
-    acc[4] = __dp2a_hi(wp, f01, acc[4]);
-    acc[5] = __dp2a_lo(wp, f23, acc[5]);
-    acc[6] = __dp2a_hi(wp, f23, acc[6]);
+// Appearance accumulation of a corner PAIR from its pair-interleaved 16-byte entry (see
+// DevScene): 7 dp2a (16-bit weights packed in wp, bytes already paired).  acc[c] is in units
+// of 1/65535 byte.
+__device__ __forceinline__ void acc_pair(uint32_t acc[7], uint4 p, uint32_t wp) {
+    acc[0] = __dp2a_lo(wp, p.x, acc[0]);
+    acc[1] = __dp2a_hi(wp, p.x, acc[1]);
+    acc[2] = __dp2a_lo(wp, p.y, acc[2]);
+    acc[3] = __dp2a_hi(wp, p.y, acc[3]);
+    acc[4] = __dp2a_lo(wp, p.z, acc[4]);
+    acc[5] = __dp2a_hi(wp, p.z, acc[5]);
+    acc[6] = __dp2a_lo(wp, p.w, acc[6]);
 }
 
 // Evaluate the field at lattice point (Qx, Qy, Qz) and composite it (Eq. 1-2, 5-7).
@@ -309,14 +305,12 @@ __device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, i
         // ---- appearance pass: 20 AoS texels, channels 1..7, the same weights + dp2a
         uint32_t acc[7] = {0u, 0u, 0u, 0u, 0u, 0u, 0u};
         if (blk >= 0) {
-            const uint2* atl = reinterpret_cast<const uint2*>(S.atlas);
-            const unsigned bbase = (unsigned)blk * 729u;   // < 2^21 * 729: 32-bit index math
+            const unsigned bbase = (unsigned)blk * 648u;   // pair entries per block: 9 z x 9 y x 8 x
             const int lx = vi[0] & 7, ly = vi[1] & 7, lz = vi[2] & 7;
 #pragma unroll
-            for (int c = 0; c < 4; c++) {                 // (dy, dz) rows; x pair per row
+            for (int c = 0; c < 4; c++) {                 // (dy, dz) rows; one x pair per row
                 const int dy = c & 1, dz = c >> 1;
-                const uint2* row = atl + (bbase + (unsigned)(((lz + dz) * 9 + (ly + dy)) * 9 + lx));
-                acc_pair(acc, __ldg(row), __ldg(row + 1), wV[c]);
+                acc_pair(acc, __ldg(S.atlas_pairs + (bbase + (unsigned)(((lz + dz) * 9 + (ly + dy)) * 8 + lx))), wV[c]);
             }
         }
 #pragma unroll
@@ -324,12 +318,9 @@ __device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, i
             if (!(ALL || S.use_p[a])) continue;
             const int ua = (a == 0) ? 1 : 0;
             const int va = (a == 2) ? 1 : 2;
-            const uint2* pl = reinterpret_cast<const uint2*>(S.planes);
 #pragma unroll
-            for (int dv = 0; dv < 2; dv++) {
-                const uint2* row = pl + (unsigned)((a * S.R + pi[va] + dv) * S.R + pi[ua]);
-                acc_pair(acc, __ldg(row), __ldg(row + 1), wP[a][dv]);
-            }
+            for (int dv = 0; dv < 2; dv++)
+                acc_pair(acc, __ldg(S.plane_pairs + (unsigned)((a * S.R + pi[va] + dv) * S.R + pi[ua])), wP[a][dv]);
         }
         // sigmoid(x), x = acc ka / 65535 - n m: 1 / (1 + 2^(-x log2e)), the exponent in one FFMA
         const float off = (float)n_src * S.ma_l2;
