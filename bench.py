@@ -322,7 +322,8 @@ def main():
             ems = float(t.item())
         e2e = {"value": total_rays / (ems / 1e3), "unit": "rays/s",
                "h2d_bytes_per_step": V * 136, "d2h_bytes_per_step": V * W_IMG * H_IMG * 4,
-               "path": "merf_render_host (C ABI, pinned host output, render/copy overlapped in chunks of 4 views)"}
+               "path": "merf_render_host (C ABI, pinned host output; device staging, each chunk's copy "
+                       "overlapped with the next chunk's render: chunks of 14 + 2 views)"}
 
     if rank == 0:
         cpu = None

@@ -209,8 +209,9 @@ merf_status merf_render_progressive(const merf_scene *scene, const merf_camera *
 
 /*
  * End-to-end variant with HOST output: renders into scene-owned device staging buffers in
- * chunks and copies each finished chunk to `out_host` [host] (pinned memory recommended)
- * while the next chunk renders.  Synchronous on return.  Same layouts/errors as merf_render.
+ * chunks (up to 14 views, then a last chunk of 2) and copies each finished chunk to
+ * `out_host` [host] (pinned memory recommended) while the next chunk renders, so only the
+ * last short copy is exposed.  Synchronous on return.  Same layouts/errors as merf_render.
  */
 merf_status merf_render_host(const merf_scene *scene, const merf_camera *cams, int32_t n_cams,
                              int32_t W, int32_t H, int32_t format, void *out_host,

@@ -602,7 +602,31 @@ extern "C" merf_status merf_render_host(const merf_scene* cs, const merf_camera*
     cudaStream_t st = (cudaStream_t)stream;
     const size_t px_bytes = format == MERF_RGBA_U8 ? 4 : 12;
     const size_t frame = (size_t)W * H * px_bytes;
-    const int chunk = 4;   // views per chunk; chunk i+1 renders while chunk i copies out
+    // Chunk plan: big chunks (efficient persistent-march launches) whose copies hide behind
+    // the next chunk's render, then a small last chunk so that only its short copy is exposed.
+    static const int kTail = [] {
+        const char* e = getenv("MERF_HOST_TAIL");
+        const int v = e ? atoi(e) : 2;
+        return v >= 1 ? v : 2;
+    }();
+    static const int kBig = [] {   // measured e2e (16 views): 4x4 960, 12+4 980, 14+2 989 M rays/s
+        const char* e = getenv("MERF_HOST_BIG");
+        const int v = e ? atoi(e) : 14;
+        return v >= 1 ? v : 14;
+    }();
+    std::vector<int> plan;
+    {
+        const int tail = n_cams < kTail ? n_cams : kTail;
+        int rem = n_cams - tail;
+        while (rem > 0) {
+            const int c = rem < kBig ? rem : kBig;
+            plan.push_back(c);
+            rem -= c;
+        }
+        plan.push_back(tail);
+    }
+    int chunk = 0;
+    for (int c : plan) chunk = c > chunk ? c : chunk;
     const size_t need = frame * chunk;
     if (s->stage_bytes < need) {
         for (int i = 0; i < 2; i++) {
@@ -620,8 +644,9 @@ extern "C" merf_status merf_render_host(const merf_scene* cs, const merf_camera*
     for (int i = 0; i < 2; i++) CUDA_TRY(cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming));
     bool pending[2] = {false, false};
     int b = 0;
-    for (int c0 = 0; c0 < n_cams; c0 += chunk, b ^= 1) {
-        int n = n_cams - c0 < chunk ? n_cams - c0 : chunk;
+    int c0 = 0;
+    for (size_t pi = 0; pi < plan.size(); c0 += plan[pi], pi++, b ^= 1) {
+        const int n = plan[pi];
         if (pending[b]) CUDA_TRY(cudaStreamWaitEvent(st, copied[b], 0));   // buffer free again
         e = render_frames(s, cams + c0, n, W, H, format, s->stage[b], flags, st, nullptr);
         if (e) return e;
