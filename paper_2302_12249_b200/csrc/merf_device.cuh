@@ -223,6 +223,18 @@ __device__ __forceinline__ bool make_segment(const DevScene& S, int g, const dou
     return true;
 }
 
+// MUFU-only exp2 / reciprocal (flush-to-zero; no range fix-up instructions)
+__device__ __forceinline__ float ex2_ftz(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float rcp_ftz(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 // ------------------------------------------------------------------------------------
 // int32 lattice helpers (F = 28: |Q| <= 2^29 + drift, so every position, cell and texel
 // coordinate fits a 32-bit register)
@@ -247,7 +259,7 @@ __device__ __forceinline__ bool occ_bit(const uint32_t* bits, int cx, int cy, in
 __device__ __forceinline__ int exit_axis(int Qa, int U, int lo, int hi, int K) {
     const int a = abs(U);
     const int num = U > 0 ? hi - Qa : Qa - lo + 1;
-    const float ef = ceilf(__fdividef((float)num, (float)a));
+    const float ef = ceilf((float)num * rcp_ftz((float)a));   // a integer: no denormal guard
     int e = (int)fminf(ef, (float)K);
     e += (e * a < num) ? 1 : 0;
     e -= ((e - 1) * a >= num) ? 1 : 0;
@@ -284,18 +296,6 @@ __device__ __forceinline__ void wsplit(uint32_t Wi, float Wf, float f, uint32_t&
 __device__ __forceinline__ uint32_t wleaf(uint32_t Wi, float Wf, float f) {
     const uint32_t t = __float_as_uint(fmaf(f, Wf, kMagicF));   // kMagicBits + w1
     return __byte_perm(Wi + kMagicBits - t, t, 0x5410);
-}
-
-// MUFU-only exp2 / reciprocal (flush-to-zero; no range fix-up instructions)
-__device__ __forceinline__ float ex2_ftz(float x) {
-    float y;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
-__device__ __forceinline__ float rcp_ftz(float x) {
-    float y;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
 }
 
 }  // namespace merf

@@ -36,6 +36,11 @@ static cudaError_t march_v(const DevScene& S, int64_t n, const Workspace& ws, ui
     return cudaGetLastError();
 }
 
+static bool env_flag(const char* name) {
+    const char* e = getenv(name);
+    return e && e[0] && e[0] != '0';
+}
+
 // the per-cell skip table is used when the scene has one, unless MERF_NO_SKIPTAB is set (tests
 // and ablations run both traversals)
 static bool use_skiptab(const DevScene& S) {
@@ -49,6 +54,10 @@ cudaError_t launch_march(int kf, const DevScene& S, int64_t n, const Workspace& 
     const bool tab = use_skiptab(S);
     if (S.n_src == 4 && !(kf & (KF_TRACE | KF_DENSE))) {    // production variants
         if (tab) {
+            if (S.L == kPaperL && S.R == kPaperR && S.n_fin == kPaperNf && !env_flag("MERF_NO_PAPER")) {
+                if (kf & KF_COUNT) return march_v<KF_ALLSRC | KF_SKIPTAB | KF_PAPER | KF_COUNT>(S, n, ws, rflags, ta, stats, st);
+                return march_v<KF_ALLSRC | KF_SKIPTAB | KF_PAPER>(S, n, ws, rflags, ta, stats, st);
+            }
             if (kf & KF_COUNT) return march_v<KF_ALLSRC | KF_SKIPTAB | KF_COUNT>(S, n, ws, rflags, ta, stats, st);
             return march_v<KF_ALLSRC | KF_SKIPTAB>(S, n, ws, rflags, ta, stats, st);
         }

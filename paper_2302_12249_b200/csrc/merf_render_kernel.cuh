@@ -34,6 +34,22 @@ enum : int {
     KF_SEGS = 32,       // record contracted segments only (no marching)
     KF_ALLSRC = 64,     // all four sources present (compile-time; the production variant)
     KF_SKIPTAB = 128,   // skip level from the per-cell table (S.skiptab) instead of the level search
+    KF_PAPER = 256,     // the paper's default resolutions as compile-time constants (below)
+};
+
+// The paper's default scene geometry (L = 512, R = 2048; finest occupancy level
+// 256^3) as compile-time constants: the shifts, strides and clamps become immediates and free
+// the registers that held them (the march kernel runs at the 64-register limit).  Selected at
+// launch when the scene has exactly this geometry; every other scene runs the generic kernel.
+constexpr int kPaperL = 512, kPaperR = 2048, kPaperNf = 256;
+template <int KF> struct Geo {
+    static __device__ __forceinline__ int L(const DevScene& S) { return (KF & KF_PAPER) ? kPaperL : S.L; }
+    static __device__ __forceinline__ int R(const DevScene& S) { return (KF & KF_PAPER) ? kPaperR : S.R; }
+    static __device__ __forceinline__ int nb(const DevScene& S) { return (KF & KF_PAPER) ? kPaperL / 8 : S.nb; }
+    static __device__ __forceinline__ int sV(const DevScene& S) { return (KF & KF_PAPER) ? kF + 2 - 9 : S.sV; }
+    static __device__ __forceinline__ int sP(const DevScene& S) { return (KF & KF_PAPER) ? kF + 2 - 11 : S.sP; }
+    static __device__ __forceinline__ int Nf(const DevScene& S) { return (KF & KF_PAPER) ? kPaperNf : S.n_fin; }
+    static __device__ __forceinline__ int sf(const DevScene& S) { return (KF & KF_PAPER) ? kF + 2 - 8 : S.s_fin; }
 };
 
 constexpr int kSetupThreads = 128;
@@ -212,6 +228,12 @@ struct RayState {
     float F[4];
 };
 
+// the ray's accumulators (C_d, T), F as stored for the shade kernel
+__device__ __forceinline__ void store_accum(float4* a, const RayState& st) {
+    a[0] = make_float4(st.cd[0], st.cd[1], st.cd[2], st.T);
+    a[1] = make_float4(st.F[0], st.F[1], st.F[2], st.F[3]);
+}
+
 
 // Appearance accumulation of a corner PAIR from its pair-interleaved 16-byte entry (see
 // DevScene): 7 dp2a (16-bit weights packed in wp, bytes already paired).  acc[c] is in units
@@ -247,8 +269,9 @@ __device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, i
     if (use_v) {
         float vf[3];
 #pragma unroll
-        for (int a = 0; a < 3; a++) texel(Q[a], S.sV, S.L, vi[a], vf[a]);
-        const int slot = ((vi[2] >> 3) * S.nb + (vi[1] >> 3)) * S.nb + (vi[0] >> 3);
+        for (int a = 0; a < 3; a++) texel(Q[a], Geo<KF>::sV(S), Geo<KF>::L(S), vi[a], vf[a]);
+        const int nb = Geo<KF>::nb(S);
+        const int slot = ((vi[2] >> 3) * nb + (vi[1] >> 3)) * nb + (vi[0] >> 3);
         if (slot != bslot) {                              // blocks change every ~8 voxels
             bslot = slot;
             bblk = __ldg(S.block_index + slot);
@@ -277,10 +300,11 @@ __device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, i
     int pi[3] = {0, 0, 0};
     uint32_t wP[3][2] = {{0u, 0u}, {0u, 0u}, {0u, 0u}};
     const bool any_p = ALL || S.R > 0;
+    const int R = Geo<KF>::R(S);
     if (any_p) {
         float pf[3];
 #pragma unroll
-        for (int a = 0; a < 3; a++) texel(Q[a], S.sP, S.R, pi[a], pf[a]);
+        for (int a = 0; a < 3; a++) texel(Q[a], Geo<KF>::sP(S), R, pi[a], pf[a]);
 #pragma unroll
         for (int a = 0; a < 3; a++) {
             if (!(ALL || S.use_p[a])) continue;
@@ -292,7 +316,7 @@ __device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, i
             wP[a][0] = wleaf(v0i, v0f, pf[ua]);
             wP[a][1] = wleaf(v1i, v1f, pf[ua]);
             // ---- density pass, plane a: the texel quad (byte du + 2 dv) as 2 dp2a
-            const uint32_t quad = __ldg(S.pdens + (unsigned)((a * S.R + pi[va]) * S.R + pi[ua]));
+            const uint32_t quad = __ldg(S.pdens + (unsigned)((a * R + pi[va]) * R + pi[ua]));
             sd = __dp2a_lo(wP[a][0], quad, sd);
             sd = __dp2a_hi(wP[a][1], quad, sd);
         }
@@ -320,7 +344,7 @@ __device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, i
             const int va = (a == 2) ? 1 : 2;
 #pragma unroll
             for (int dv = 0; dv < 2; dv++)
-                acc_pair(acc, __ldg(S.plane_pairs + (unsigned)((a * S.R + pi[va] + dv) * S.R + pi[ua])), wP[a][dv]);
+                acc_pair(acc, __ldg(S.plane_pairs + (unsigned)((a * R + pi[va] + dv) * R + pi[ua])), wP[a][dv]);
         }
         // sigmoid(x), x = acc ka / 65535 - n m: 1 / (1 + 2^(-x log2e)), the exponent in one FFMA
         const float off = (float)n_src * S.ma_l2;
@@ -351,8 +375,8 @@ __global__ void __launch_bounds__(kMarchThreads, 4) march_kernel(DevScene S, int
     const int lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
     const int nl = S.n_levels;
-    const int Nf = S.n_fin;
-    const int sf = S.s_fin;
+    const int Nf = Geo<KF>::Nf(S);
+    const int sf = Geo<KF>::sf(S);
     const uint32_t* occ_f = S.occ_fin;
     const bool early_term = !(rflags & MERF_NO_EARLY_TERM);
 
@@ -368,9 +392,7 @@ __global__ void __launch_bounds__(kMarchThreads, 4) march_kernel(DevScene S, int
     int c_eval = 0, c_donly = 0, c_skip = 0, c_miss = 0, c_rounds = 0, c_steps = 0, c_lanes = 0;
 
     auto finish = [&]() {
-        float4* a = ws.accum + (int64_t)ray * 2;
-        a[0] = make_float4(st.cd[0], st.cd[1], st.cd[2], st.T);
-        a[1] = make_float4(st.F[0], st.F[1], st.F[2], st.F[3]);
+        store_accum(ws.accum + (int64_t)ray * 2, st);
         if (KF & KF_TRACE) ta.counts[ray] = n_eval;
         ray = -1;
     };
@@ -630,9 +652,7 @@ __global__ void __launch_bounds__(kSetupThreads) march_sph_kernel(DevScene S, Ra
         }
     }
     if (r < rs.n) {
-        float4* a = ws.accum + r * 2;
-        a[0] = make_float4(st.cd[0], st.cd[1], st.cd[2], st.T);
-        a[1] = make_float4(st.F[0], st.F[1], st.F[2], st.F[3]);
+        store_accum(ws.accum + r * 2, st);
         if (KF & KF_TRACE) ta.counts[ray] = n_eval;
     }
     if (KF & KF_COUNT) {

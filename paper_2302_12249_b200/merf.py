@@ -14,7 +14,9 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmerf.so")
+# MERF_LIB: another in-tree build of the same library (A/B timing of kernel variants, e.g.
+# `tools/ab_bench.sh`); default: the library next to this file
+LIB_PATH = os.environ.get("MERF_LIB") or os.path.join(_HERE, "libmerf.so")
 
 MERF_OK, MERF_EINVAL, MERF_ENOMEM, MERF_ECUDA, MERF_ENCCL, MERF_EMISMATCH, MERF_EIO = range(7)
 MERF_RGB_F32, MERF_RGBA_U8 = 0, 1
