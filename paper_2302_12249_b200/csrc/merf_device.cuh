@@ -22,6 +22,7 @@ constexpr int kTwoI = 1 << (kF + 1);                      // contracted 2.0 (int
 constexpr int kMaxSeg = 7;                                // convex regions: <= 7 per ray
 constexpr int kMaxCams = 16;                              // cameras per launch (kernel params)
 constexpr int kMlpFloats = 883;
+constexpr int kMlpFragWords = 44;                         // per-lane words of the mma MLP table
 
 struct DevScene {
     // appearance layouts, pair-interleaved along the fastest axis: entry (.., u) holds texels u
@@ -40,6 +41,8 @@ struct DevScene {
     // finest level; NULL when that level is too large for it (then the level search runs).
     const uint32_t* skiptab;
     const float* mlp;             // [883]
+    // per-lane mma fragments of the MLP (merf_shade_mma.cu); NULL = FFMA shade kernel
+    const uint32_t* mlp_frag;     // [32][kMlpFragWords]
     int L, R, nb, n_levels;
     int level_res[MERF_MAX_LEVELS];
     int level_shift[MERF_MAX_LEVELS];   // F + 2 - log2(N)
@@ -239,8 +242,11 @@ __device__ __forceinline__ float rcp_ftz(float x) {
 // int32 lattice helpers (F = 28: |Q| <= 2^29 + drift, so every position, cell and texel
 // coordinate fits a 32-bit register)
 // ------------------------------------------------------------------------------------
-__device__ __forceinline__ int occ_cell(int Q, int shift, int N) {
-    int c = (Q + kTwoI) >> shift;
+// Lattice positions in the kernels are BIASED by contracted 2.0: Qb = Q + 2^(F+1), so the
+// contracted cube [-2, 2)^3 maps to [0, 2^(F+2)) and a cell / texel index is a plain shift.
+// (The workspace segments store biased origins; merf_segment records keep the unbiased Qa.)
+__device__ __forceinline__ int occ_cell(int Qb, int shift, int N) {
+    int c = Qb >> shift;
     return min(max(c, 0), N - 1);
 }
 
@@ -249,6 +255,9 @@ __device__ __forceinline__ bool occ_bit(const uint32_t* bits, int cx, int cy, in
     uint32_t w = __ldg(bits + (lin >> 5));
     return (w >> (lin & 31)) & 1u;
 }
+
+constexpr float kMagicF = 12582912.f;          // 1.5 * 2^23
+constexpr uint32_t kMagicBits = 0x4B400000u;   // its bit pattern (low 22 bits zero)
 
 // First k' >= 0 with Qa + k' U outside [lo, hi) along one axis, capped at K.  Both signs
 // reduce to e = ceil(num / |U|) with num = hi - Qa (U > 0) or Qa - lo + 1 (U < 0), num >= 1
@@ -259,8 +268,11 @@ __device__ __forceinline__ bool occ_bit(const uint32_t* bits, int cx, int cy, in
 __device__ __forceinline__ int exit_axis(int Qa, int U, int lo, int hi, int K) {
     const int a = abs(U);
     const int num = U > 0 ? hi - Qa : Qa - lo + 1;
-    const float ef = ceilf((float)num * rcp_ftz((float)a));   // a integer: no denormal guard
-    int e = (int)fminf(ef, (float)K);
+    // ceil of the estimate num * rcp(a) in one FFMA rounding up onto the integer grid of the
+    // 1.5 * 2^23 magic (exact below 2^22; positive float bit patterns are monotonic, so any larger,
+    // infinite or NaN quotient (a = 0) still clamps to K): no FRND / F2I on the XU pipe
+    const float t = __fmaf_ru((float)num, rcp_ftz((float)a), kMagicF);
+    int e = min((int)(__float_as_uint(t) - kMagicBits), K);
     e += (e * a < num) ? 1 : 0;
     e -= ((e - 1) * a >= num) ? 1 : 0;
     return min(e, K);
@@ -271,8 +283,8 @@ __device__ __forceinline__ int exit_axis(int Qa, int U, int lo, int hi, int K) {
 // [texel 0, texel M-1] gives the same interpolated value as the (M-2, f = 1) convention at
 // the upper edge: the extra corner i0 + 1 = M carries weight 0 (the layouts are padded so
 // that it is a valid address).
-__device__ __forceinline__ void texel(int Q, int s, int M, int& i0, float& f) {
-    const int P = min(max(Q + kTwoI - (1 << (s - 1)), 0), (M - 1) << s);
+__device__ __forceinline__ void texel(int Qb, int s, int M, int& i0, float& f) {
+    const int P = min(max(Qb - (1 << (s - 1)), 0), (M - 1) << s);
     i0 = P >> s;
     f = (float)(P & ((1 << s) - 1)) * __int_as_float((127 - s) << 23);
 }
@@ -282,8 +294,6 @@ __device__ __forceinline__ void texel(int Q, int s, int M, int& i0, float& f) {
 // into (W - round(f W), round(f W)).  The rounding is one FFMA against the 1.5 * 2^23 magic
 // (t = f W + M leaves round(f W) in the low mantissa bits: no F2I), and every weight is
 // carried both as an int and as an exact float so the next split needs no conversion.
-constexpr float kMagicF = 12582912.f;          // 1.5 * 2^23
-constexpr uint32_t kMagicBits = 0x4B400000u;   // its bit pattern (low 22 bits zero)
 __device__ __forceinline__ void wsplit(uint32_t Wi, float Wf, float f, uint32_t& w0i, float& w0f, uint32_t& w1i,
                                        float& w1f) {
     const float t = fmaf(f, Wf, kMagicF);

@@ -39,7 +39,7 @@ struct QatArgs {
 __device__ __forceinline__ void coord_qat(int Q, int M, int& i0, float& f) {
     // lower texel index in [0, M-2] and fraction (cell-centred, clamp to edge; reading D9)
     const int s = kF + 2 - (31 - __clz(M));
-    const int P = Q + kTwoI - (1 << (s - 1));
+    const int P = Q - (1 << (s - 1));          // Q biased (workspace segments, see occ_cell)
     int i = P >> s;
     float fr = (float)(P & ((1 << s) - 1)) * __int_as_float((127 - s) << 23);
     if (i < 0) { i = 0; fr = 0.f; }

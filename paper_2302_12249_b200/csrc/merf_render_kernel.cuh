@@ -137,7 +137,7 @@ __device__ __forceinline__ void emit_segment(const DevScene& S, int g, const dou
         }
     } else if (nseg < kMaxSeg) {
         int4* p = ws.seg + (r * kMaxSeg + nseg) * 2;
-        p[0] = make_int4(sg.Qa[0], sg.Qa[1], sg.Qa[2], sg.K);
+        p[0] = make_int4(sg.Qa[0] + kTwoI, sg.Qa[1] + kTwoI, sg.Qa[2] + kTwoI, sg.K);   // biased origin
         p[1] = make_int4(sg.U[0], sg.U[1], sg.U[2], sg.region);
     }
     nseg++;
@@ -504,9 +504,9 @@ __global__ void __launch_bounds__(kMarchThreads, 4) march_kernel(DevScene S, int
                 // one convergent exit computation for every skipping lane: jump to the first
                 // lattice sample outside that empty cell (ray-AABB exit)
                 const int K = qa.w;
-                e = min(K, exit_axis(qa.x, uu.x, (cx << sh) - kTwoI, ((cx + 1) << sh) - kTwoI, K));
-                e = min(e, exit_axis(qa.y, uu.y, (cy << sh) - kTwoI, ((cy + 1) << sh) - kTwoI, K));
-                e = min(e, exit_axis(qa.z, uu.z, (cz << sh) - kTwoI, ((cz + 1) << sh) - kTwoI, K));
+                e = min(K, exit_axis(qa.x, uu.x, cx << sh, (cx + 1) << sh, K));
+                e = min(e, exit_axis(qa.y, uu.y, cy << sh, (cy + 1) << sh, K));
+                e = min(e, exit_axis(qa.z, uu.z, cz << sh, (cz + 1) << sh, K));
             }
             if (e >= 0) {
                 k = min(max(k + 1, e), qa.w);
@@ -630,9 +630,9 @@ __global__ void __launch_bounds__(kSetupThreads) march_sph_kernel(DevScene S, Ra
             const double rad = contract_sph(x, c);
             const double cr = rad <= 1.0 ? rad : sub_rn(2.0, div_rn(1.0, rad));
             if (cr >= stop) break;
-            const int Qx = (int)__double2ll_rn(mul_rn(c[0], (double)kOne));
-            const int Qy = (int)__double2ll_rn(mul_rn(c[1], (double)kOne));
-            const int Qz = (int)__double2ll_rn(mul_rn(c[2], (double)kOne));
+            const int Qx = (int)__double2ll_rn(mul_rn(c[0], (double)kOne)) + kTwoI;   // biased
+            const int Qy = (int)__double2ll_rn(mul_rn(c[1], (double)kOne)) + kTwoI;
+            const int Qz = (int)__double2ll_rn(mul_rn(c[2], (double)kOne)) + kTwoI;
             const int fx = occ_cell(Qx, sf, Nf), fy = occ_cell(Qy, sf, Nf), fz = occ_cell(Qz, sf, Nf);
             if (occ_bit(S.occ_fin, fx, fy, fz, Nf)) {
                 const int kind = shade_sample<KF>(S, Qx, Qy, Qz, st, bslot, bblk);
