@@ -165,6 +165,7 @@ def run_reference(args):
             "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "orbit1080p_paper_scale_merf" + ("_dense_ablation" if args.dense else "")
+                        + ("_mlp_ffma_ablation" if getattr(args, "mlp_ffma", False) else "")
                                    + ("_spherical_contraction" if args.spherical else ""), "scene": "c2 (512^3 sparse grid, 3x2048^2 planes)",
                        "sample": f"every {stride}th pixel of one 1920x1080 orbit view per step"},
             "cpu_baseline": {"value": value, "unit": "rays/s", "cores": O.max_threads(), "kind": "oracle",
@@ -189,6 +190,8 @@ def main():
                          "rendered with fixed contracted-arc-length steps and no AABB skipping")
     ap.add_argument("--dense", action="store_true",
                     help="ablation: dense lattice stepping gated by the finest level (no skipping)")
+    ap.add_argument("--mlp-ffma", action="store_true",
+                    help="ablation: the deferred MLP as FFMA chains instead of the tensor-core kernel")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -215,7 +218,8 @@ def main():
     steps_total = args.warmup + args.steps
     batches = [orbit_cameras(N_ORBIT, indices=views_for(rank, world, s, V)) for s in range(steps_total)]
 
-    extra_flags = (M.MERF_DENSE if args.dense else 0) | (M.MERF_SPHERICAL if args.spherical else 0)
+    extra_flags = ((M.MERF_DENSE if args.dense else 0) | (M.MERF_SPHERICAL if args.spherical else 0)
+                   | (M.MERF_MLP_FFMA if args.mlp_ffma else 0))
     stream = torch.cuda.Stream()
     gstream = torch.cuda.Stream()
     frames = [torch.empty((V, H_IMG, W_IMG, 4), dtype=torch.uint8, device=dev) for _ in range(2)]
@@ -335,6 +339,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": "orbit1080p_paper_scale_merf" + ("_dense_ablation" if args.dense else "")
+                        + ("_mlp_ffma_ablation" if getattr(args, "mlp_ffma", False) else "")
                                    + ("_spherical_contraction" if args.spherical else ""),
                        "views_per_rank_per_step": V, "W": W_IMG, "H": H_IMG,
                        "scene": {k: info[k] for k in ("L", "R", "level_res", "n_blocks", "device_bytes")},

@@ -68,12 +68,16 @@ enum {
     MERF_COUNTERS = 2u,        /* accumulate merf_stats (adds device atomics)             */
     MERF_DENSE = 4u,           /* debug: dense stepping gated by the finest level only     */
     MERF_TIMED = 8u,           /* record CUDA events around every pipeline kernel launch     */
-    MERF_SPHERICAL = 16u       /* NEXT-2 comparison variant: the scene's grids live in the
+    MERF_SPHERICAL = 16u,      /* NEXT-2 comparison variant: the scene's grids live in the
                                   space of the spherical contraction of Eq. 4;
                                   fixed contracted-arc-length Euler steps, t += Delta/sigma(t),
                                   every sample tested against the finest level, no AABB skip
                                   (P:222-226).  Accepted by merf_render, merf_render_rays,
                                   merf_trace (segment ordinal 0, k = step index).            */
+    MERF_MLP_FFMA = 32u        /* run the deferred MLP (Eq. 3) as FFMA chains instead of
+                                  the default tensor-core kernel (split-fp16 mma.sync, fp32-class
+                                  accuracy); cross-check / ablation.  Scenes whose MLP weights
+                                  could overflow fp16 always use the FFMA kernel.              */
 };
 
 #define MERF_MAX_LEVELS 4

@@ -150,6 +150,27 @@ static void fill_dev(merf_scene* s) {
     S.alpha_skip = d.alpha_skip;
 }
 
+// Bound on every operand the tensor-core MLP (merf_shade_mma.cu) converts to fp16: the inputs
+// are in [-1, 1] (C_d, F in [0, 1] since sum w <= 1; |d| = 1; sin, cos), so layer l's
+// pre-activations are bounded by max_o |b_o| + sum_i |W_oi| * (bound of layer l - 1).
+// NaN/inf weights give +inf (FFMA kernel).
+static double mlp_mma_bound(const float* w) {
+    const int nin[3] = {34, 16, 16}, nout[3] = {16, 16, 3}, woff[3] = {0, 560, 832}, boff[3] = {544, 816, 880};
+    double in = 1.0, worst = 1.0;
+    for (int l = 0; l < 3; l++) {
+        double m = 0.0;
+        for (int o = 0; o < nout[l]; o++) {
+            double a = fabs((double)w[boff[l] + o]);
+            for (int i = 0; i < nin[l]; i++) a += fabs((double)w[woff[l] + o * nin[l] + i]) * in;
+            if (!(a <= 1e30)) return INFINITY;
+            m = fmax(m, a);
+        }
+        in = m;
+        worst = fmax(worst, m);
+    }
+    return worst;
+}
+
 template <typename T>
 static merf_status dalloc(merf_scene* s, T** p, size_t bytes) {
     void* q = nullptr;
@@ -222,6 +243,13 @@ extern "C" merf_status merf_scene_upload(const merf_scene_desc* desc, const uint
     UPC_TRY(cudaMemcpyAsync(d_mlp, mlp, kMlpFloats * sizeof(float), cudaMemcpyHostToDevice, cs));
     S.mlp = d_mlp;
     memcpy(s->mlp_params.w, mlp, sizeof(s->mlp_params.w));
+    S.mlp_frag = nullptr;
+    if (mlp_mma_bound(mlp) < 3e4) {        // fp16 operand range of the tensor-core MLP
+        uint32_t* d_frag;
+        UP_TRY(dalloc(s, &d_frag, 32 * kMlpFragWords * sizeof(uint32_t)));
+        UPC_TRY(launch_mlp_frag(d_mlp, d_frag, cs));
+        S.mlp_frag = d_frag;
+    }
     // ---- planes
     if (use_p) {
         size_t pb = (size_t)3 * desc->R * desc->R * 8;
@@ -466,7 +494,8 @@ static cudaError_t call_march_sph(void* p) {
 }
 static cudaError_t call_shade(void* p) {
     ChunkCall* c = (ChunkCall*)p;
-    return launch_shade(c->kf_shade, c->s->dev, *c->rs, *c->ws, c->out, c->s->mlp_params, c->st);
+    return launch_shade(c->kf_shade, c->s->dev, *c->rs, *c->ws, c->out, c->s->mlp_params,
+                        (c->flags & MERF_MLP_FFMA) != 0, c->st);
 }
 
 static merf_status run_chunk(const merf_scene* s, int kf_setup, int kf_march, int kf_shade,

@@ -18,7 +18,11 @@ cudaError_t launch_march(int kf, const DevScene& S, int64_t n, const Workspace& 
 cudaError_t launch_march_sph(int kf, const DevScene& S, const RaySource& rs, const Workspace& ws,
                              uint32_t rflags, const TraceArgs& ta, unsigned long long* stats, cudaStream_t st);
 cudaError_t launch_shade(int kf, const DevScene& S, const RaySource& rs, const Workspace& ws, void* out,
-                         const MlpParams& mlp, cudaStream_t st);
+                         const MlpParams& mlp, bool ffma, cudaStream_t st);
+// deferred MLP on the tensor cores (merf_shade_mma.cu; needs S.mlp_frag)
+cudaError_t launch_shade_mma(int kf, const DevScene& S, const RaySource& rs, const Workspace& ws, void* out,
+                             cudaStream_t st);
+cudaError_t launch_mlp_frag(const float* w, uint32_t* frag, cudaStream_t st);
 
 // K0: coarse[N^3 bits] = OR over each (f/N)^3 block of fine[f^3 bits]
 cudaError_t launch_maxpool_bits(const uint32_t* fine, int f, uint32_t* coarse, int N, cudaStream_t st);

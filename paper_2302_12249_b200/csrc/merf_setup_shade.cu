@@ -35,7 +35,10 @@ static cudaError_t shade_v(const DevScene& S, const RaySource& rs, const Workspa
 }
 
 cudaError_t launch_shade(int kf, const DevScene& S, const RaySource& rs, const Workspace& ws, void* out,
-                         const MlpParams& mlp, cudaStream_t st) {
+                         const MlpParams& mlp, bool ffma, cudaStream_t st) {
+    // the tensor-core MLP when the scene has its fragment table (activation bound checked at
+    // upload), unless the caller asked for the FFMA kernel (MERF_MLP_FFMA)
+    if (S.mlp_frag && !ffma) return launch_shade_mma(kf, S, rs, ws, out, st);
     switch (kf & (KF_RAYS | KF_U8)) {
         case 0: return shade_v<0>(S, rs, ws, out, mlp, st);
         case KF_U8: return shade_v<KF_U8>(S, rs, ws, out, mlp, st);

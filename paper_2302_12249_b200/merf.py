@@ -20,7 +20,7 @@ LIB_PATH = os.environ.get("MERF_LIB") or os.path.join(_HERE, "libmerf.so")
 
 MERF_OK, MERF_EINVAL, MERF_ENOMEM, MERF_ECUDA, MERF_ENCCL, MERF_EMISMATCH, MERF_EIO = range(7)
 MERF_RGB_F32, MERF_RGBA_U8 = 0, 1
-MERF_NO_EARLY_TERM, MERF_COUNTERS, MERF_DENSE, MERF_TIMED, MERF_SPHERICAL = 1, 2, 4, 8, 16
+MERF_NO_EARLY_TERM, MERF_COUNTERS, MERF_DENSE, MERF_TIMED, MERF_SPHERICAL, MERF_MLP_FFMA = 1, 2, 4, 8, 16, 32
 MAX_LEVELS = 4
 
 _STATUS = {1: "MERF_EINVAL", 2: "MERF_ENOMEM", 3: "MERF_ECUDA", 4: "MERF_ENCCL", 5: "MERF_EMISMATCH", 6: "MERF_EIO"}

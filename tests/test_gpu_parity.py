@@ -517,3 +517,73 @@ def test_skip_table_equals_level_search(M, c2):
     assert stats[0]["density_only"] == stats[1]["density_only"]
     assert stats[0]["skips"] <= stats[1]["skips"]
     assert np.array_equal(traces[0][0], traces[1][0]) and np.array_equal(traces[0][1], traces[1][1])
+
+
+# ------------------------------------------------------------------------------------
+# deferred MLP on the tensor cores (merf_shade_mma.cu) vs the FFMA kernel and the oracle
+# ------------------------------------------------------------------------------------
+# split-fp16 products (hi*hi + hi*lo + lo*hi, fp32 accumulation) drop terms of ~2^-22 relative;
+# through three 16-wide layers with |W| <= 0.3 the logits agree with fp32 FFMA chains to ~1e-6
+MMA_VS_FFMA = 2e-5
+
+
+def test_mlp_mma_matches_ffma_and_oracle(M, c1_scene, c2):
+    import dataclasses
+    cams, W, H = config_cameras("c1")
+    a, _ = _gpu_frame(M, c1_scene, cams, W, H)
+    b, _ = _gpu_frame(M, c1_scene, cams, W, H, flags=M.MERF_MLP_FFMA)
+    assert np.abs(a - b).max() <= MMA_VS_FFMA
+    ref = O.render(O.OracleScene(c1_scene), cams[0], W, H)
+    assert np.abs(a[0].reshape(-1, 3) - ref["rgb"]).max() <= TOL
+    # paper-scale scene, two orbit views, ragged tiles (1080 = 270 x 4 rows, 1920 = 240 x 8)
+    oc = orbit_cameras(256, indices=[3, 77])
+    a, _ = _gpu_frame(M, c2, oc, 1920, 1080)
+    b, _ = _gpu_frame(M, c2, oc, 1920, 1080, flags=M.MERF_MLP_FFMA)
+    assert np.abs(a - b).max() <= MMA_VS_FFMA
+    # a ragged frame (partial 8x4 tiles: lanes without a pixel still join the warp's mma)
+    cam = look_at_camera(np.array([0.1, 0.05, -0.2]), target=np.zeros(3), W=37, H=29, fov_x_deg=60)
+    a, _ = _gpu_frame(M, c1_scene, cam[None], 37, 29)
+    b, _ = _gpu_frame(M, c1_scene, cam[None], 37, 29, flags=M.MERF_MLP_FFMA)
+    assert np.abs(a - b).max() <= MMA_VS_FFMA
+    # larger weights (exactly scaled by 4; hidden activations of tens to hundreds): still inside
+    # the fp16 operand bound, still fp32-class
+    big = dataclasses.replace(c1_scene, mlp=c1_scene.mlp * 4.0)
+    a, _ = _gpu_frame(M, big, cams, W, H)
+    b, _ = _gpu_frame(M, big, cams, W, H, flags=M.MERF_MLP_FFMA)
+    assert np.abs(a - b).max() <= 10 * MMA_VS_FFMA
+    ref = O.render(O.OracleScene(big), cams[0], W, H)
+    assert np.abs(a[0].reshape(-1, 3) - ref["rgb"]).max() <= TOL
+
+
+def test_mlp_fp16_overflow_bound_falls_back_to_ffma(M, c1_scene):
+    """weights whose activation bound exceeds the fp16 range: the upload keeps no fragment
+    table and every render runs the FFMA kernel (identical with and without the flag)."""
+    import dataclasses
+    cams, W, H = config_cameras("c1")
+    huge = dataclasses.replace(c1_scene, mlp=c1_scene.mlp * 2048.0)
+    a, _ = _gpu_frame(M, huge, cams, W, H)
+    b, _ = _gpu_frame(M, huge, cams, W, H, flags=M.MERF_MLP_FFMA)
+    assert np.array_equal(a, b)
+
+
+def test_mlp_mma_rays_and_u8(M, c1_scene):
+    import torch
+    rng = np.random.default_rng(11)
+    n = 1001                                    # ragged: the last warp is partly empty
+    o = rng.uniform(-1.2, 1.2, (n, 3))
+    d = rng.normal(size=(n, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    s = M.Scene(c1_scene)
+    outs = []
+    for fl in (0, M.MERF_MLP_FFMA):
+        rgb = torch.zeros((n, 3), dtype=torch.float32, device="cuda")
+        M.merf_render_rays(s.handle, torch.as_tensor(o, device="cuda"), torch.as_tensor(d, device="cuda"),
+                           rgb, flags=fl)
+        torch.cuda.synchronize()
+        outs.append(rgb.cpu().numpy())
+    s.close()
+    assert np.abs(outs[0] - outs[1]).max() <= MMA_VS_FFMA
+    cams, W, H = config_cameras("c1")
+    f32, _ = _gpu_frame(M, c1_scene, cams, W, H)
+    u8, _ = _gpu_frame(M, c1_scene, cams, W, H, fmt=M.MERF_RGBA_U8)
+    assert np.array_equal(u8[..., :3], np.rint(f32 * 255).astype(np.uint8))
