@@ -179,11 +179,14 @@ __device__ __forceinline__ void boundary_candidates(const double o[3], const dou
                                  {5, 6}, {8, 9}, {10, 11}, {8, 10}, {9, 11}, {9, 10}, {0, 8}, {4, 8},
                                  {2, 10}, {6, 10}, {2, 4}, {6, 8}, {1, 9}, {5, 9}, {3, 11}, {7, 11},
                                  {3, 5}, {7, 9}, {1, 2}, {3, 4}, {5, 6}, {7, 8}, {9, 10}};
+    // compare-exchange by one compare + selects: the candidates are never NaN (non-finite ones
+    // were set to +inf above), so fmin/fmax's NaN handling is dead weight
 #pragma unroll
     for (int c = 0; c < 41; c++) {
         const double a = cand[kNet[c][0]], b = cand[kNet[c][1]];
-        cand[kNet[c][0]] = fmin(a, b);
-        cand[kNet[c][1]] = fmax(a, b);
+        const bool lt = a < b;
+        cand[kNet[c][0]] = lt ? a : b;
+        cand[kNet[c][1]] = lt ? b : a;
     }
 }
 

@@ -85,9 +85,16 @@ struct RaySource {
 __device__ __forceinline__ bool ray_pixel(const RaySource& rs, int64_t ray, int& view, int& px, int& py) {
     const int64_t tile = ray >> 5;
     const int lane = (int)(ray & 31);
-    view = (int)(tile / rs.tiles_per_view);
-    const int tt = (int)(tile - (int64_t)view * rs.tiles_per_view);
-    const int ty = tt / rs.tiles_x, tx = tt - ty * rs.tiles_x;
+    int tt;
+    if (tile <= 0xffffffffll) {            // every practical batch: 32-bit unsigned division
+        const unsigned t32 = (unsigned)tile, v = t32 / (unsigned)rs.tiles_per_view;
+        view = (int)v;
+        tt = (int)(t32 - v * (unsigned)rs.tiles_per_view);
+    } else {
+        view = (int)(tile / rs.tiles_per_view);
+        tt = (int)(tile - (int64_t)view * rs.tiles_per_view);
+    }
+    const int ty = (int)((unsigned)tt / (unsigned)rs.tiles_x), tx = tt - ty * rs.tiles_x;
     const int lx = tx * 8 + (lane & 7), ly = ty * 4 + (lane >> 3);
     px = lx * rs.stride_m1 + lx + rs.ox;
     py = ly * rs.stride_m1 + ly + rs.oy;

@@ -113,21 +113,24 @@ def test_ptxas_has_no_spills(M):
     """the production kernels stay (essentially) in registers: shade none, the timed march
     variant at most one spilled register (it runs at the 64-register cap that gives 4
     CTAs/SM, measured faster than 80 registers / 3 CTAs), debug/counter variants a few more;
-    the fp64 setup kernel may save a few bytes around the IEEE division slow-path call."""
+    the fp64 setup kernel may save a few bytes around the IEEE division slow-path call (the
+    production variant <0> none; the per-ray trace variant <1> a few more)."""
     import sys
     sys.path.insert(0, os.path.join(ROOT, "tools"))
     from ptxas_summary import parse
     info = parse()
     assert any(k.startswith("march_kernel") for k in info)
     for k, v in info.items():
-        if k.startswith("shade_kernel"):
+        if k.startswith("shade_kernel") or k.startswith("shade_mma_kernel"):
             assert v["spill_st"] == 0 and v["spill_ld"] == 0 and v["stack"] == 0, (k, v)
         elif k in ("march_kernel<0>", "march_kernel<16>"):
             assert v["spill_st"] <= 8 and v["regs"] <= 64, (k, v)
         elif k.startswith("march_kernel"):
             assert v["spill_st"] <= 64, (k, v)
+        elif k == "setup_kernel<0>":
+            assert v["spill_st"] == 0 and v["stack"] == 0, (k, v)
         elif k.startswith("setup_kernel"):
-            assert v["spill_st"] <= 16, (k, v)
+            assert v["spill_st"] <= 32, (k, v)
 
 
 def test_product_package_does_not_touch_oracle():
