@@ -242,6 +242,21 @@ __device__ __forceinline__ void store_accum(float4* a, const RayState& st) {
 }
 
 
+// Linear index of texel (v, u) of plane a in the [3][R][R] layouts.  With the paper geometry
+// the fields are disjoint bit ranges, so one 32-bit OR chain (the plane offset never becomes
+// a separate 64-bit pointer add).
+template <int KF>
+__device__ __forceinline__ unsigned plane_index(int a, int R, int v, int u) {
+    if (KF & KF_PAPER) {
+        // opaque to the compiler: it would otherwise peel the plane offset off into a 64-bit
+        // pointer add (IADD3 + IMAD.X per access) after the 32-bit index scaling
+        unsigned idx;
+        asm("lop3.b32 %0, %1, %2, %3, 0xfe;" : "=r"(idx) : "r"((unsigned)a << 22), "r"((unsigned)v << 11), "r"((unsigned)u));
+        return idx;
+    }
+    return (unsigned)((a * R + v) * R + u);
+}
+
 // Appearance accumulation of a corner PAIR from its pair-interleaved 16-byte entry (see
 // DevScene): 7 dp2a (16-bit weights packed in wp, bytes already paired).  acc[c] is in units
 // of 1/65535 byte.
@@ -323,7 +338,7 @@ __device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, i
             wP[a][0] = wleaf(v0i, v0f, pf[ua]);
             wP[a][1] = wleaf(v1i, v1f, pf[ua]);
             // ---- density pass, plane a: the texel quad (byte du + 2 dv) as 2 dp2a
-            const uint32_t quad = __ldg(S.pdens + (unsigned)((a * R + pi[va]) * R + pi[ua]));
+            const uint32_t quad = __ldg(S.pdens + plane_index<KF>(a, R, pi[va], pi[ua]));
             sd = __dp2a_lo(wP[a][0], quad, sd);
             sd = __dp2a_hi(wP[a][1], quad, sd);
         }
@@ -336,12 +351,14 @@ __device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, i
         // ---- appearance pass: 20 AoS texels, channels 1..7, the same weights + dp2a
         uint32_t acc[7] = {0u, 0u, 0u, 0u, 0u, 0u, 0u};
         if (blk >= 0) {
-            const unsigned bbase = (unsigned)blk * 648u;   // pair entries per block: 9 z x 9 y x 8 x
             const int lx = vi[0] & 7, ly = vi[1] & 7, lz = vi[2] & 7;
+            // pair entries per block: 9 z x 9 y x 8 x; the four (dy, dz) rows as constant
+            // offsets from one pointer (immediate LDG offsets, one address computation)
+            const uint4* row = S.atlas_pairs + ((unsigned)blk * 648u + (unsigned)((lz * 9 + ly) * 8 + lx));
 #pragma unroll
             for (int c = 0; c < 4; c++) {                 // (dy, dz) rows; one x pair per row
                 const int dy = c & 1, dz = c >> 1;
-                acc_pair(acc, __ldg(S.atlas_pairs + (bbase + (unsigned)(((lz + dz) * 9 + (ly + dy)) * 8 + lx))), wV[c]);
+                acc_pair(acc, __ldg(row + (dz * 72 + dy * 8)), wV[c]);
             }
         }
 #pragma unroll
@@ -349,9 +366,9 @@ __device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, i
             if (!(ALL || S.use_p[a])) continue;
             const int ua = (a == 0) ? 1 : 0;
             const int va = (a == 2) ? 1 : 2;
+            const uint4* row = S.plane_pairs + plane_index<KF>(a, R, pi[va], pi[ua]);
 #pragma unroll
-            for (int dv = 0; dv < 2; dv++)
-                acc_pair(acc, __ldg(S.plane_pairs + (unsigned)((a * R + pi[va] + dv) * R + pi[ua])), wP[a][dv]);
+            for (int dv = 0; dv < 2; dv++) acc_pair(acc, __ldg(row + dv * R), wP[a][dv]);
         }
         // sigmoid(x), x = acc ka / 65535 - n m: 1 / (1 + 2^(-x log2e)), the exponent in one FFMA
         const float off = (float)n_src * S.ma_l2;
