@@ -292,6 +292,19 @@ __device__ __forceinline__ void texel(int Qb, int s, int M, int& i0, float& f) {
     f = (float)(P & ((1 << s) - 1)) * __int_as_float((127 - s) << 23);
 }
 
+// The same texel coordinate with the fraction delivered as g = 2^23 + f 2^s, an exact float
+// built by one LOP3 (needs s <= 23; the compile-time paper geometry has s = 21, 19): no I2F and
+// no scaling multiply.  g_frac recovers f exactly (power-of-two scaling, one FFMA).
+__device__ __forceinline__ float exp2i(int n) { return __int_as_float((127 + n) << 23); }
+__device__ __forceinline__ void texel_g(int Qb, int s, int M, int& i0, float& g) {
+    const int P = min(max(Qb - (1 << (s - 1)), 0), (M - 1) << s);
+    i0 = P >> s;
+    unsigned b;                        // (P & mask) | 0x4B000000 in one LOP3
+    asm("lop3.b32 %0, %1, %2, %3, 0xea;" : "=r"(b) : "r"(P), "r"((1 << s) - 1), "r"(0x4B000000));
+    g = __uint_as_float(b);
+}
+__device__ __forceinline__ float g_frac(float g, int s) { return fmaf(g, exp2i(-s), -exp2i(23 - s)); }
+
 // 16-bit fixed-point interpolation weights that partition 65535 EXACTLY (so a constant
 // field interpolates exactly): split an integer weight W along one axis with fraction f
 // into (W - round(f W), round(f W)).  The rounding is one FFMA against the 1.5 * 2^23 magic
@@ -304,6 +317,15 @@ __device__ __forceinline__ void wsplit(uint32_t Wi, float Wf, float f, uint32_t&
     w0i = Wi - w1i;
     w1f = t - kMagicF;
     w0f = Wf - w1f;
+}
+// the first split of the full weight 65535 straight from g: f 65535 + M = g (65535 2^-s) +
+// (M - 65535 2^(23-s)), both constants exact, so t is bit-identical to wsplit's
+__device__ __forceinline__ void wsplit_full_g(float g, int s, uint32_t& w0i, float& w0f, uint32_t& w1i, float& w1f) {
+    const float t = fmaf(g, 65535.f * exp2i(-s), kMagicF - 65535.f * exp2i(23 - s));
+    w1i = __float_as_uint(t) - kMagicBits;
+    w0i = 65535u - w1i;
+    w1f = t - kMagicF;
+    w0f = 65535.f - w1f;
 }
 // the last split, packed as the (lo16, hi16) = (W - w1, w1) operand of dp2a: FFMA, IADD3, PRMT
 __device__ __forceinline__ uint32_t wleaf(uint32_t Wi, float Wf, float f) {

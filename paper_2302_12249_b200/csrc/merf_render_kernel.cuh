@@ -288,10 +288,16 @@ __device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, i
     int vi[3] = {0, 0, 0};
     uint32_t wV[4] = {0u, 0u, 0u, 0u};
     int blk = -1;
+    // compile-time geometry: fractions as exact g-floats (texel_g), no I2F / scaling
+    constexpr bool GF = (KF & KF_PAPER) != 0;
     if (use_v) {
-        float vf[3];
+        float vf[3], vg[3];
+        const int sV = Geo<KF>::sV(S);
 #pragma unroll
-        for (int a = 0; a < 3; a++) texel(Q[a], Geo<KF>::sV(S), Geo<KF>::L(S), vi[a], vf[a]);
+        for (int a = 0; a < 3; a++) {
+            if (GF) texel_g(Q[a], sV, Geo<KF>::L(S), vi[a], vg[a]);
+            else texel(Q[a], sV, Geo<KF>::L(S), vi[a], vf[a]);
+        }
         const int nb = Geo<KF>::nb(S);
         const int slot = ((vi[2] >> 3) * nb + (vi[1] >> 3)) * nb + (vi[0] >> 3);
         if (slot != bslot) {                              // blocks change every ~8 voxels
@@ -301,12 +307,30 @@ __device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, i
         blk = bblk;
         uint32_t zi[2], yi[4];
         float zf[2], yf[4];
-        wsplit(65535u, 65535.f, vf[2], zi[0], zf[0], zi[1], zf[1]);
+        if (GF) {
+            wsplit_full_g(vg[2], sV, zi[0], zf[0], zi[1], zf[1]);
+            vf[1] = g_frac(vg[1], sV);
+            vf[0] = g_frac(vg[0], sV);
+        } else {
+            wsplit(65535u, 65535.f, vf[2], zi[0], zf[0], zi[1], zf[1]);
+        }
         wsplit(zi[0], zf[0], vf[1], yi[0], yf[0], yi[1], yf[1]);
         wsplit(zi[1], zf[1], vf[1], yi[2], yf[2], yi[3], yf[3]);
 #pragma unroll
         for (int c = 0; c < 4; c++) wV[c] = wleaf(yi[c], yf[c], vf[0]);
-        if (blk >= 0) {
+        if (ALL) {
+            // branch-free: a missing block (impossible in a scene that passed the upload's
+            // soundness check, but defined: it contributes nothing) reads block 0 with zero
+            // weights, so neither pass needs a divergent region around the V gather
+            if (blk < 0) {
+                n_src -= 1;
+                ret = 2;
+#pragma unroll
+                for (int c = 0; c < 4; c++) wV[c] = 0u;
+            }
+            blk = max(blk, 0);
+        }
+        if (ALL || blk >= 0) {
             // ---- density pass, V: the corner octet (byte c = dx + 2 dy + 4 dz) as 4 dp2a
             const uint2 oct = __ldg(S.vdens + (unsigned)(blk * 512 + ((vi[2] & 7) * 8 + (vi[1] & 7)) * 8 + (vi[0] & 7)));
             sd = __dp2a_lo(wV[0], oct.x, sd);
@@ -324,9 +348,17 @@ __device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, i
     const bool any_p = ALL || S.R > 0;
     const int R = Geo<KF>::R(S);
     if (any_p) {
-        float pf[3];
+        float pf[3], pg[3];
+        const int sP = Geo<KF>::sP(S);
 #pragma unroll
-        for (int a = 0; a < 3; a++) texel(Q[a], Geo<KF>::sP(S), R, pi[a], pf[a]);
+        for (int a = 0; a < 3; a++) {
+            if (GF) {
+                texel_g(Q[a], sP, R, pi[a], pg[a]);
+                pf[a] = g_frac(pg[a], sP);      // used only as a u axis (x, y); dead for z
+            } else {
+                texel(Q[a], sP, R, pi[a], pf[a]);
+            }
+        }
 #pragma unroll
         for (int a = 0; a < 3; a++) {
             if (!(ALL || S.use_p[a])) continue;
@@ -334,7 +366,8 @@ __device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, i
             const int va = (a == 2) ? 1 : 2;
             uint32_t v0i, v1i;
             float v0f, v1f;
-            wsplit(65535u, 65535.f, pf[va], v0i, v0f, v1i, v1f);
+            if (GF) wsplit_full_g(pg[va], sP, v0i, v0f, v1i, v1f);
+            else wsplit(65535u, 65535.f, pf[va], v0i, v0f, v1i, v1f);
             wP[a][0] = wleaf(v0i, v0f, pf[ua]);
             wP[a][1] = wleaf(v1i, v1f, pf[ua]);
             // ---- density pass, plane a: the texel quad (byte du + 2 dv) as 2 dp2a
@@ -350,7 +383,7 @@ __device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, i
     if (alpha > S.alpha_skip) {
         // ---- appearance pass: 20 AoS texels, channels 1..7, the same weights + dp2a
         uint32_t acc[7] = {0u, 0u, 0u, 0u, 0u, 0u, 0u};
-        if (blk >= 0) {
+        if (ALL || blk >= 0) {
             const int lx = vi[0] & 7, ly = vi[1] & 7, lz = vi[2] & 7;
             // pair entries per block: 9 z x 9 y x 8 x; the four (dy, dz) rows as constant
             // offsets from one pointer (immediate LDG offsets, one address computation)
