@@ -310,27 +310,39 @@ __device__ __forceinline__ float g_frac(float g, int s) { return fmaf(g, exp2i(-
 // into (W - round(f W), round(f W)).  The rounding is one FFMA against the 1.5 * 2^23 magic
 // (t = f W + M leaves round(f W) in the low mantissa bits: no F2I), and every weight is
 // carried both as an int and as an exact float so the next split needs no conversion.
+//
+// Integer weights that feed a LEAF split are carried BIASED, Wb = W - 65535 M (mod 2^32), so the
+// leaf packs its dp2a operand with one IMAD: with t = M + w1 (bits of the leaf's FFMA),
+// 65535 t + Wb = W + 65535 w1 = (W - w1) + (w1 << 16) -- lo16 = W - w1, hi16 = w1 (both in
+// [0, 65535], no carry).  B selects the biased form of a split's two children.
+constexpr uint32_t kLeafBias = 65535u * kMagicBits;   // mod 2^32
+template <bool B = false>
 __device__ __forceinline__ void wsplit(uint32_t Wi, float Wf, float f, uint32_t& w0i, float& w0f, uint32_t& w1i,
                                        float& w1f) {
     const float t = fmaf(f, Wf, kMagicF);
-    w1i = __float_as_uint(t) - kMagicBits;
-    w0i = Wi - w1i;
+    const uint32_t tb = __float_as_uint(t);
+    w1i = tb - (kMagicBits + (B ? kLeafBias : 0u));
+    w0i = Wi - tb + (kMagicBits - (B ? kLeafBias : 0u));
     w1f = t - kMagicF;
     w0f = Wf - w1f;
 }
 // the first split of the full weight 65535 straight from g: f 65535 + M = g (65535 2^-s) +
 // (M - 65535 2^(23-s)), both constants exact, so t is bit-identical to wsplit's
+template <bool B = false>
 __device__ __forceinline__ void wsplit_full_g(float g, int s, uint32_t& w0i, float& w0f, uint32_t& w1i, float& w1f) {
     const float t = fmaf(g, 65535.f * exp2i(-s), kMagicF - 65535.f * exp2i(23 - s));
-    w1i = __float_as_uint(t) - kMagicBits;
-    w0i = 65535u - w1i;
+    const uint32_t tb = __float_as_uint(t);
+    w1i = tb - (kMagicBits + (B ? kLeafBias : 0u));
+    w0i = (65535u + kMagicBits - (B ? kLeafBias : 0u)) - tb;
     w1f = t - kMagicF;
     w0f = 65535.f - w1f;
 }
-// the last split, packed as the (lo16, hi16) = (W - w1, w1) operand of dp2a: FFMA, IADD3, PRMT
-__device__ __forceinline__ uint32_t wleaf(uint32_t Wi, float Wf, float f) {
+// the last split of a BIASED weight Wb, packed as the (lo16, hi16) = (W - w1, w1) operand of
+// dp2a: FFMA + IMAD (the multiply-add runs on the FMA pipe; the ALU pipe is the march's
+// busiest)
+__device__ __forceinline__ uint32_t wleaf(uint32_t Wb, float Wf, float f) {
     const uint32_t t = __float_as_uint(fmaf(f, Wf, kMagicF));   // kMagicBits + w1
-    return __byte_perm(Wi + kMagicBits - t, t, 0x5410);
+    return t * 65535u + Wb;
 }
 
 }  // namespace merf

@@ -314,8 +314,8 @@ __device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, i
         } else {
             wsplit(65535u, 65535.f, vf[2], zi[0], zf[0], zi[1], zf[1]);
         }
-        wsplit(zi[0], zf[0], vf[1], yi[0], yf[0], yi[1], yf[1]);
-        wsplit(zi[1], zf[1], vf[1], yi[2], yf[2], yi[3], yf[3]);
+        wsplit<true>(zi[0], zf[0], vf[1], yi[0], yf[0], yi[1], yf[1]);   // leaf parents: biased
+        wsplit<true>(zi[1], zf[1], vf[1], yi[2], yf[2], yi[3], yf[3]);
 #pragma unroll
         for (int c = 0; c < 4; c++) wV[c] = wleaf(yi[c], yf[c], vf[0]);
         if (ALL) {
@@ -366,8 +366,8 @@ __device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, i
             const int va = (a == 2) ? 1 : 2;
             uint32_t v0i, v1i;
             float v0f, v1f;
-            if (GF) wsplit_full_g(pg[va], sP, v0i, v0f, v1i, v1f);
-            else wsplit(65535u, 65535.f, pf[va], v0i, v0f, v1i, v1f);
+            if (GF) wsplit_full_g<true>(pg[va], sP, v0i, v0f, v1i, v1f);
+            else wsplit<true>(65535u, 65535.f, pf[va], v0i, v0f, v1i, v1f);
             wP[a][0] = wleaf(v0i, v0f, pf[ua]);
             wP[a][1] = wleaf(v1i, v1f, pf[ua]);
             // ---- density pass, plane a: the texel quad (byte du + 2 dv) as 2 dp2a

@@ -1,5 +1,5 @@
 """Aggregate an ncu report's source page by CUDA source line (stall samples, executed
-instructions).  usage: python tools/ncu_lines.py report.ncu-rep [top]"""
+instructions).  usage: python tools/ncu_lines.py report.ncu-rep [top] [kernel-regex]"""
 import csv
 import subprocess
 import sys
@@ -8,7 +8,8 @@ import sys
 def main():
     rep = sys.argv[1]
     top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
-    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--print-source", "cuda,sass", "--csv"],
+    kf = ["-k", "regex:" + sys.argv[3]] if len(sys.argv) > 3 else []
+    out = subprocess.run(["ncu", "-i", rep, *kf, "--page", "source", "--print-source", "cuda,sass", "--csv"],
                          capture_output=True, text=True).stdout
     rows = []
     path = None

@@ -1,5 +1,5 @@
 """Key metrics of an ncu report (details page) as `name = value unit` lines.
-usage: python tools/ncu_summary.py report.ncu-rep"""
+usage: python tools/ncu_summary.py report.ncu-rep [kernel-regex]"""
 import csv
 import subprocess
 import sys
@@ -14,7 +14,8 @@ KEYS = ["Duration", "Elapsed Cycles", "SM Frequency", "Registers Per Thread", "T
 
 
 def main():
-    out = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "details", "--csv"], capture_output=True,
+    kf = ["-k", "regex:" + sys.argv[2]] if len(sys.argv) > 2 else []
+    out = subprocess.run(["ncu", "-i", sys.argv[1], *kf, "--page", "details", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(out.splitlines()))
     hdr = rows[0]
@@ -26,7 +27,7 @@ def main():
         if r[iname] in KEYS and r[iname] not in seen:
             seen.add(r[iname])
             print(f"{r[iname]:45s} = {r[ival]} {r[iunit]}")
-    raw = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv"], capture_output=True,
+    raw = subprocess.run(["ncu", "-i", sys.argv[1], *kf, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout.splitlines()
     if len(raw) >= 3:
         h = next(csv.reader([raw[0]]))

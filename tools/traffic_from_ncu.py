@@ -14,8 +14,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("report")
     ap.add_argument("--out", default="profiles/render_traffic.json")
+    ap.add_argument("--kernel", default="march_kernel", help="kernel-name regex (report may hold several)")
     a = ap.parse_args()
-    out = subprocess.run(["ncu", "-i", a.report, "--page", "raw", "--csv", "--print-units", "base", "--metrics",
+    out = subprocess.run(["ncu", "-i", a.report, "-k", "regex:" + a.kernel, "--page", "raw", "--csv", "--print-units", "base", "--metrics",
                           "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum"],
                          capture_output=True, text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
