@@ -280,9 +280,9 @@ extern "C" merf_status merf_scene_upload(const merf_scene_desc* desc, const uint
     for (int i = 0; i < MERF_MAX_LEVELS; i++) S.occ[i] = d_occ[i < nl ? i : nl - 1];
     S.occ_fin = d_occ[nl - 1];
     S.skiptab = nullptr;
-    if (Nf <= kSkipTabMaxRes && Nf >= 2) {    // 4 bits per finest cell (64 MB at 512^3)
+    if (Nf <= kSkipTabMaxRes && Nf >= 2) {    // 1 byte per bordered finest cell (136 MB at 512^3)
         uint32_t* d_tab;
-        UP_TRY(dalloc(s, &d_tab, (size_t)Nf * Nf * Nf / 2));
+        UP_TRY(dalloc(s, &d_tab, (size_t)skiptab_words(Nf) * 4));
         UPC_TRY(launch_skiptab(d_occ[nl - 1], Nf, d_tab, cs));
         S.skiptab = d_tab;
     }

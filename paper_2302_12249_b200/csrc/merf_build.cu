@@ -341,7 +341,8 @@ cudaError_t launch_contract(const double* x, int64_t n, double* y, int32_t* regi
 // OR-pools of the finest level at every power-of-two resolution N_f/2, ..., 1 -- the
 // multi-level occupancy grid of P:307-308 completed to all scales, so each skip leaves the
 // largest aligned empty cell around the sample.  Only empty space is skipped, so the set of
-// evaluated samples (and every trace) is the one of dense stepping.  One thread per 8 cells.
+// evaluated samples (and every trace) is the one of dense stepping.  One byte per entry, one
+// thread per 4 entries.
 // ------------------------------------------------------------------------------------
 constexpr int kMaxDyadic = 16;
 struct LevelSet {
@@ -349,16 +350,25 @@ struct LevelSet {
     int n;
 };
 
+// The table is BORDERED: (N + 2)^3 entries, entry (x + 1, y + 1, z + 1) for cell (x, y, z) and
+// a one-cell border that repeats the clamped edge cell, so the march indexes it with the
+// unclamped cell Qb >> s_fin (lattice drift never leaves the cube by a whole finest cell).
 __global__ void skiptab_kernel(LevelSet ls, uint32_t* __restrict__ tab) {
     const int nl = ls.n;
     const int N = 1 << (nl - 1);
-    const int64_t words = (int64_t)N * N * N / 8;
+    const int Nb = N + 2;
+    const int64_t entries = (int64_t)Nb * Nb * Nb;
+    const int64_t words = (entries + 3) / 4;
     const int64_t wi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (wi >= words) return;
     uint32_t out = 0;
-    for (int q = 0; q < 8; q++) {
-        const int64_t c = wi * 8 + q;
-        const int x = (int)(c % N), y = (int)((c / N) % N), z = (int)(c / ((int64_t)N * N));
+    for (int q = 0; q < 4; q++) {
+        const int64_t e = wi * 4 + q;
+        if (e >= entries) break;
+        const int x = min(max((int)(e % Nb) - 1, 0), N - 1);
+        const int y = min(max((int)((e / Nb) % Nb) - 1, 0), N - 1);
+        const int z = min(max((int)(e / ((int64_t)Nb * Nb)) - 1, 0), N - 1);
+        const int64_t c = ((int64_t)z * N + y) * N + x;
         uint32_t code = 0;
         if (!((__ldg(ls.occ[nl - 1] + (c >> 5)) >> (c & 31)) & 1u)) {
             int lev = nl - 1;                    // the finest (known empty) unless a coarser one is
@@ -372,7 +382,7 @@ __global__ void skiptab_kernel(LevelSet ls, uint32_t* __restrict__ tab) {
             }
             code = (uint32_t)(kF + 2 - lev - 16);   // lattice shift of resolution 2^lev, - 16
         }
-        out |= code << (4 * q);
+        out |= code << (8 * q);
     }
     tab[wi] = out;
 }
@@ -394,7 +404,7 @@ cudaError_t launch_skiptab(const uint32_t* finest, int Nf, uint32_t* tab, cudaSt
         ls.occ[l] = tmp[l];
     }
     if (e == cudaSuccess) {
-        const int64_t words = (int64_t)Nf * Nf * Nf / 8;
+        const int64_t words = skiptab_words(Nf);
         skiptab_kernel<<<(unsigned)((words + 255) / 256), 256, 0, st>>>(ls, tab);
         e = cudaGetLastError();
     }

@@ -37,8 +37,9 @@ struct DevScene {
     const uint32_t* occ_fin;      // = occ[n_levels - 1] (static offset: no dynamic param indexing)
     int n_fin, s_fin;             // = level_res / level_shift of the finest level
     // per finest cell, the lattice shift of the coarsest EMPTY dyadic cell containing it,
-    // minus 16 (4-bit codes, 8 per word, x fastest); 0 = occupied.  Derived exactly from the
-    // finest level; NULL when that level is too large for it (then the level search runs).
+    // minus 16 (one byte per entry, x fastest, over the (N_f + 2)^3 BORDERED grid whose border
+    // repeats the clamped edge cells); 0 = occupied.  Derived exactly from the finest level;
+    // NULL when that level is too large for it (then the level search runs).
     const uint32_t* skiptab;
     const float* mlp;             // [883]
     // per-lane mma fragments of the MLP (merf_shade_mma.cu); NULL = FFMA shade kernel

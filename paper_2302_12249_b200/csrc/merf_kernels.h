@@ -45,7 +45,9 @@ cudaError_t launch_pack_atlas(const uint8_t* dense, int L, const int32_t* index,
 // appearance pair layouts from the AoS planes / atlas (see DevScene)
 cudaError_t launch_pack_pairs(const uint8_t* planes, int R, uint4* plane_pairs, const uint8_t* atlas,
                               int64_t n_blocks, uint4* atlas_pairs, cudaStream_t st);
-// skip table of the march (one 4-bit code per finest cell over all dyadic levels; Nf >= 2)
+// skip table of the march (one 4-bit code per finest cell over all dyadic levels; Nf >= 2),
+// bordered: (Nf + 2)^3 entries (see merf_build.cu)
+inline int64_t skiptab_words(int Nf) { const int64_t b = Nf + 2; return (b * b * b + 3) / 4; }
 cudaError_t launch_skiptab(const uint32_t* finest, int Nf, uint32_t* tab, cudaStream_t st);
 cudaError_t launch_contract(const double* x, int64_t n, double* y, int32_t* region, cudaStream_t st);
 

@@ -508,6 +508,28 @@ __global__ void __launch_bounds__(kMarchThreads, 4) march_kernel(DevScene S, int
             Qx = qa.x + k * uu.x;
             Qy = qa.y + k * uu.y;
             Qz = qa.z + k * uu.z;
+            if (KF & KF_SKIPTAB) {
+                // bordered skip table: the unclamped finest cell indexes it directly (no clamps;
+                // multiply-adds on the FMA pipe).  fcell holds this entry index as the cell key.
+                const int Nb = Nf + 2;
+                fcell = ((Qz >> sf) * Nb + (Qy >> sf)) * Nb + (Qx >> sf) + (Nb * Nb + Nb + 1);
+                if (fcell == last_cell) { found = true; continue; }  // same finest cell: all levels set
+                // one probe: 0 = occupied, else the shift of the coarsest empty level - 16
+                const unsigned code = __ldg(reinterpret_cast<const uint8_t*>(S.skiptab) + (unsigned)fcell);
+                if (code == 0u) { found = true; continue; }
+                const int sh = (int)code + 16;
+                const int N = 1 << (kF + 2 - sh);
+                const int cx = occ_cell(Qx, sh, N), cy = occ_cell(Qy, sh, N), cz = occ_cell(Qz, sh, N);
+                // one convergent exit computation for every skipping lane: jump to the first
+                // lattice sample outside that empty cell (ray-AABB exit)
+                const int K = qa.w;
+                int e = min(K, exit_axis(qa.x, uu.x, cx << sh, (cx + 1) << sh, K));
+                e = min(e, exit_axis(qa.y, uu.y, cy << sh, (cy + 1) << sh, K));
+                e = min(e, exit_axis(qa.z, uu.z, cz << sh, (cz + 1) << sh, K));
+                k = min(max(k + 1, e), K);
+                if (KF & KF_COUNT) c_skip++;
+                continue;
+            }
             const int fx = occ_cell(Qx, sf, Nf), fy = occ_cell(Qy, sf, Nf), fz = occ_cell(Qz, sf, Nf);
             fcell = (fz * Nf + fy) * Nf + fx;
             if (KF & KF_DENSE) {
@@ -516,43 +538,29 @@ __global__ void __launch_bounds__(kMarchThreads, 4) march_kernel(DevScene S, int
                 continue;
             }
             if (fcell == last_cell) { found = true; continue; }  // same finest cell: all levels set
-            // finest level first: an occupied finest cell means every coarser (max-pooled) cell
-            // is occupied too, so the sample is evaluated after one probe; only an empty finest
-            // cell searches coarse -> fine for the coarsest empty level, whose cell exit is the
-            // skip target of P:308 (identical result to probing coarse -> fine throughout)
+            // level search (no skip table): finest level first -- an occupied finest cell means
+            // every coarser (max-pooled) cell is occupied too, so the sample is evaluated after
+            // one probe; only an empty finest cell searches coarse -> fine for the coarsest empty
+            // level, whose cell exit is the skip target of P:308 (identical result to probing
+            // coarse -> fine throughout)
             int e = -1;
-            bool skip;
             int sh = sf, cx = fx, cy = fy, cz = fz;
-            if (KF & KF_SKIPTAB) {
-                // one probe: 0 = occupied, else the shift of the coarsest empty level - 16
-                const unsigned code =
-                    (__ldg(S.skiptab + ((unsigned)fcell >> 3)) >> (((unsigned)fcell & 7u) * 4u)) & 15u;
-                skip = code != 0u;
-                if (skip) {
-                    sh = (int)code + 16;
-                    const int N = 1 << (kF + 2 - sh);
-                    cx = occ_cell(Qx, sh, N);
-                    cy = occ_cell(Qy, sh, N);
-                    cz = occ_cell(Qz, sh, N);
-                }
-            } else {
-                skip = !occ_bit(occ_f, fx, fy, fz, Nf);
-                if (skip) {
-                    // coarsest empty level (default: the finest, known empty)
-                    bool chosen = false;
+            const bool skip = !occ_bit(occ_f, fx, fy, fz, Nf);
+            if (skip) {
+                // coarsest empty level (default: the finest, known empty)
+                bool chosen = false;
 #pragma unroll
-                    for (int lev = 0; lev < MERF_MAX_LEVELS - 1; lev++) {
-                        if (lev < nl - 1 && !chosen) {
-                            const int N = S.level_res[lev];
-                            const int shl = S.level_shift[lev];
-                            const int x = occ_cell(Qx, shl, N), y = occ_cell(Qy, shl, N), z = occ_cell(Qz, shl, N);
-                            if (!occ_bit(S.occ[lev], x, y, z, N)) {
-                                sh = shl;
-                                cx = x;
-                                cy = y;
-                                cz = z;
-                                chosen = true;
-                            }
+                for (int lev = 0; lev < MERF_MAX_LEVELS - 1; lev++) {
+                    if (lev < nl - 1 && !chosen) {
+                        const int N = S.level_res[lev];
+                        const int shl = S.level_shift[lev];
+                        const int x = occ_cell(Qx, shl, N), y = occ_cell(Qy, shl, N), z = occ_cell(Qz, shl, N);
+                        if (!occ_bit(S.occ[lev], x, y, z, N)) {
+                            sh = shl;
+                            cx = x;
+                            cy = y;
+                            cz = z;
+                            chosen = true;
                         }
                     }
                 }
@@ -590,7 +598,10 @@ __global__ void __launch_bounds__(kMarchThreads, 4) march_kernel(DevScene S, int
             if (KF & KF_TRACE) {
                 if (n_eval < ta.max_per_ray) {
                     const int64_t idx = (int64_t)ray * ta.max_per_ray + n_eval;
-                    ta.cells[idx] = ((uint64_t)j << 61) | ((uint64_t)k << 40) | (uint64_t)fcell;
+                    const int tcell = (KF & KF_SKIPTAB)   // fcell is the bordered table index there
+                        ? (occ_cell(Qz, sf, Nf) * Nf + occ_cell(Qy, sf, Nf)) * Nf + occ_cell(Qx, sf, Nf)
+                        : fcell;
+                    ta.cells[idx] = ((uint64_t)j << 61) | ((uint64_t)k << 40) | (uint64_t)tcell;
                     if (ta.T) ta.T[idx] = st.T;
                 }
             }
