@@ -559,8 +559,7 @@ static merf_status render_frames(const merf_scene* s, const merf_camera* cams, i
         Wl = (W - prog->ox + prog->stride - 1) / prog->stride;
         Hl = (H - prog->oy + prog->stride - 1) / prog->stride;
     }
-    rs.tiles_x = (Wl + 7) / 8;
-    rs.tiles_per_view = rs.tiles_x * ((Hl + 3) / 4);
+    set_tiles(rs, (Wl + 7) / 8, ((Wl + 7) / 8) * ((Hl + 3) / 4));
     const int64_t rays_per_view = (int64_t)rs.tiles_per_view * 32;
     const int cv = chunk_views();
     int vpc = (int)(kChunkRays * cv / kViewsPerChunk / rays_per_view);
@@ -885,8 +884,7 @@ extern "C" merf_status merf_qat_step(const merf_qat_desc* d, const float* theta_
     RaySource rs{};
     rs.W = W;
     rs.H = H;
-    rs.tiles_x = (W + 7) / 8;
-    rs.tiles_per_view = rs.tiles_x * ((H + 3) / 4);
+    set_tiles(rs, (W + 7) / 8, ((W + 7) / 8) * ((H + 3) / 4));
     rs.n = (int64_t)rs.tiles_per_view * 32 * n_cams;
     if (rs.n * d->max_samples > (int64_t(1) << 31)) return fail(MERF_EINVAL, "n_rays * max_samples > 2^31");
     rs.cb.n = n_cams;

@@ -18,6 +18,7 @@
 //     C = clamp(C_d + h), store RGB f32 or RGBA8.
 #pragma once
 #include <cstdint>
+#include <climits>
 #include <cuda_runtime.h>
 
 #include "merf_device.cuh"
@@ -80,21 +81,36 @@ struct RaySource {
     // lattice.  Zero-initialised = every pixel (stride 1).
     int stride_m1, ox, oy;
     int fill;                    // shade: also write the colour to the stride x stride block
+    // exact division by tiles_per_view / tiles_x as a 64-bit multiply-high: m = ceil(2^64 / d)
+    // gives floor(n / d) = umulhi(n, m) for all n, d < 2^32 (d >= 2); 0 = not set (divide)
+    uint64_t m_tpv, m_tx;
 };
+
+// host: the tile geometry of a camera chunk and its division magics
+inline void set_tiles(RaySource& rs, int tiles_x, int tiles_per_view) {
+    rs.tiles_x = tiles_x;
+    rs.tiles_per_view = tiles_per_view;
+    rs.m_tx = tiles_x >= 2 ? UINT64_MAX / (uint64_t)tiles_x + 1 : 0;
+    rs.m_tpv = tiles_per_view >= 2 ? UINT64_MAX / (uint64_t)tiles_per_view + 1 : 0;
+}
+
+__device__ __forceinline__ unsigned div_magic(unsigned n, unsigned d, uint64_t m) {
+    return m ? (unsigned)__umul64hi((uint64_t)n, m) : n / d;
+}
 
 __device__ __forceinline__ bool ray_pixel(const RaySource& rs, int64_t ray, int& view, int& px, int& py) {
     const int64_t tile = ray >> 5;
     const int lane = (int)(ray & 31);
     int tt;
-    if (tile <= 0xffffffffll) {            // every practical batch: 32-bit unsigned division
-        const unsigned t32 = (unsigned)tile, v = t32 / (unsigned)rs.tiles_per_view;
+    if (tile <= 0xffffffffll) {            // every practical batch: 32-bit, by multiply-high
+        const unsigned t32 = (unsigned)tile, v = div_magic(t32, (unsigned)rs.tiles_per_view, rs.m_tpv);
         view = (int)v;
         tt = (int)(t32 - v * (unsigned)rs.tiles_per_view);
     } else {
         view = (int)(tile / rs.tiles_per_view);
         tt = (int)(tile - (int64_t)view * rs.tiles_per_view);
     }
-    const int ty = (int)((unsigned)tt / (unsigned)rs.tiles_x), tx = tt - ty * rs.tiles_x;
+    const int ty = (int)div_magic((unsigned)tt, (unsigned)rs.tiles_x, rs.m_tx), tx = tt - ty * rs.tiles_x;
     const int lx = tx * 8 + (lane & 7), ly = ty * 4 + (lane >> 3);
     px = lx * rs.stride_m1 + lx + rs.ox;
     py = ly * rs.stride_m1 + ly + rs.oy;
@@ -188,10 +204,12 @@ __global__ void __launch_bounds__(kSetupThreads) setup_kernel(DevScene S, RaySou
 #pragma unroll
             for (int q = 0; q < 12; q++) sc[q] = cand[q];
             double b = t_near, seg_start = t_near;
-            int g_cur = -1, ci = 0;
-            for (int it = 0; it < 13; it++) {
-                while (ci < 12 && sc[ci] <= b) ci++;
-                const double nb = ci < 12 ? sc[ci] : __longlong_as_double(0x7ff0000000000000ll);
+            int g_cur = -1;
+            for (int q = 0; q <= 12; q++) {
+                // the sorted candidates in order, one shared-memory load each; a repeat of the
+                // previous boundary (two planes crossed at the same t) adds no interval
+                const double nb = q < 12 ? sc[q] : __longlong_as_double(0x7ff0000000000000ll);
+                if (!(nb > b)) continue;
                 const bool last = isinf(nb);
                 const double p = last ? add_rn(mul_rn(b, 2.0), 1.0) : mul_rn(add_rn(b, nb), 0.5);
                 double x[3];

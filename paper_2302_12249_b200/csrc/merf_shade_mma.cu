@@ -138,8 +138,8 @@ __global__ void __launch_bounds__(128) shade_mma_kernel(DevScene S, RaySource rs
             valid = ray_pixel(rs, ray, view, px, py);
             if (valid) {
                 const merf_camera& c = rs.cb.cam[view];
-                const float x0 = ((float)px + 0.5f - (float)c.cx) / (float)c.fx;
-                const float x1 = ((float)py + 0.5f - (float)c.cy) / (float)c.fy;
+                const float x0 = __fdividef((float)px + 0.5f - (float)c.cx, (float)c.fx);   // an MLP input:
+                const float x1 = __fdividef((float)py + 0.5f - (float)c.cy, (float)c.fy);   // ~1 ulp is plenty
                 float v[3];
 #pragma unroll
                 for (int q = 0; q < 3; q++)
