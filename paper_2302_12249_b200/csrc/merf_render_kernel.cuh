@@ -507,21 +507,16 @@ __global__ void __launch_bounds__(kMarchThreads, 4) march_kernel(DevScene S, int
         // skip chain never idles the rest of the warp.
         bool found = false;
         int Qx = 0, Qy = 0, Qz = 0, fcell = 0;
-        for (int it = 0; it < tune.trav_steps; it++) {
-            const bool want = ray >= 0 && !found;
-            const unsigned m_want = __ballot_sync(FULL, want);
-            if (m_want == 0) break;
-            if (KF & KF_COUNT) c_steps += lane == 0;
-            if (it > 0 && __popc(act & ~m_want) >= tune.shade_min) break;   // lanes ready to shade
-            if (!want) continue;
+        // one traversal step of a lane that wants a sample
+        auto step = [&]() {
             if (k >= qa.w) {                                  // segment exhausted
                 j++;
-                if (j >= ns) { finish(); continue; }
+                if (j >= ns) { finish(); return; }
                 const int4* p = ws.seg + ((int64_t)ray * kMaxSeg + j) * 2;
                 qa = p[0];
                 uu = p[1];
                 k = 0;
-                continue;
+                return;
             }
             Qx = qa.x + k * uu.x;
             Qy = qa.y + k * uu.y;
@@ -531,10 +526,10 @@ __global__ void __launch_bounds__(kMarchThreads, 4) march_kernel(DevScene S, int
                 // multiply-adds on the FMA pipe).  fcell holds this entry index as the cell key.
                 const int Nb = Nf + 2;
                 fcell = ((Qz >> sf) * Nb + (Qy >> sf)) * Nb + (Qx >> sf) + (Nb * Nb + Nb + 1);
-                if (fcell == last_cell) { found = true; continue; }  // same finest cell: all levels set
+                if (fcell == last_cell) { found = true; return; }  // same finest cell: all levels set
                 // one probe: 0 = occupied, else the shift of the coarsest empty level - 16
                 const unsigned code = __ldg(reinterpret_cast<const uint8_t*>(S.skiptab) + (unsigned)fcell);
-                if (code == 0u) { found = true; continue; }
+                if (code == 0u) { found = true; return; }
                 const int sh = (int)code + 16;
                 const int N = 1 << (kF + 2 - sh);
                 const int cx = occ_cell(Qx, sh, N), cy = occ_cell(Qy, sh, N), cz = occ_cell(Qz, sh, N);
@@ -546,16 +541,16 @@ __global__ void __launch_bounds__(kMarchThreads, 4) march_kernel(DevScene S, int
                 e = min(e, exit_axis(qa.z, uu.z, cz << sh, (cz + 1) << sh, K));
                 k = min(max(k + 1, e), K);
                 if (KF & KF_COUNT) c_skip++;
-                continue;
+                return;
             }
             const int fx = occ_cell(Qx, sf, Nf), fy = occ_cell(Qy, sf, Nf), fz = occ_cell(Qz, sf, Nf);
             fcell = (fz * Nf + fy) * Nf + fx;
             if (KF & KF_DENSE) {
                 if (occ_bit(occ_f, fx, fy, fz, Nf)) found = true;
                 else k++;
-                continue;
+                return;
             }
-            if (fcell == last_cell) { found = true; continue; }  // same finest cell: all levels set
+            if (fcell == last_cell) { found = true; return; }  // same finest cell: all levels set
             // level search (no skip table): finest level first -- an occupied finest cell means
             // every coarser (max-pooled) cell is occupied too, so the sample is evaluated after
             // one probe; only an empty finest cell searches coarse -> fine for the coarsest empty
@@ -567,7 +562,7 @@ __global__ void __launch_bounds__(kMarchThreads, 4) march_kernel(DevScene S, int
             if (skip) {
                 // coarsest empty level (default: the finest, known empty)
                 bool chosen = false;
-#pragma unroll
+    #pragma unroll
                 for (int lev = 0; lev < MERF_MAX_LEVELS - 1; lev++) {
                     if (lev < nl - 1 && !chosen) {
                         const int N = S.level_res[lev];
@@ -597,6 +592,18 @@ __global__ void __launch_bounds__(kMarchThreads, 4) march_kernel(DevScene S, int
             } else {
                 found = true;
             }
+        };
+        // the first step runs for every lane holding a ray (none has found a sample yet);
+        // further steps only while lanes still search and fewer than shade_min are ready
+        if (KF & KF_COUNT) c_steps += lane == 0;
+        if (ray >= 0) step();
+        for (int it = 1; it < tune.trav_steps; it++) {
+            const bool want = ray >= 0 && !found;
+            const unsigned m_want = __ballot_sync(FULL, want);
+            if (m_want == 0) break;
+            if (KF & KF_COUNT) c_steps += lane == 0;
+            if (__popc(act & ~m_want) >= tune.shade_min) break;   // lanes ready to shade
+            if (want) step();
         }
 
         // ---------------- shading (converged) ----------------
