@@ -107,13 +107,34 @@ def _peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def _ncu_traffic():
-    """dram bytes per launch of the render kernel from the committed ncu --set full capture."""
+def _ncu_capture():
+    """per-launch counters of the march kernel from the committed ncu --set full capture
+    (profiles/render_traffic.json, written by tools/traffic_from_ncu.py)."""
     try:
         with open(os.path.join(ROOT, "profiles", "render_traffic.json")) as f:
-            return json.load(f).get("dram_bytes_per_launch")
+            return json.load(f)
     except Exception:
+        return {}
+
+
+def _ncu_traffic():
+    """dram bytes per launch of the render kernel from the committed ncu --set full capture."""
+    return _ncu_capture().get("dram_bytes_per_launch")
+
+
+def issue_roofline(avg_launch_ms: float, sm_mhz: float, n_sm: int):
+    """The limiter of the march kernel: instruction issue.  achieved = warp instructions per
+    launch (ncu, same launch configuration) / (live launch time x SM clock x SMs), against 4
+    (one issue per cycle per SM sub-partition)."""
+    cap = _ncu_capture()
+    inst = cap.get("warp_inst_per_launch")
+    if not inst or not avg_launch_ms or not sm_mhz:
         return None
+    ipc = inst / (avg_launch_ms * 1e-3 * sm_mhz * 1e6 * n_sm)
+    return {"bound": "issue", "achieved": ipc, "peak": 4.0, "unit": "warp inst / cycle / SM",
+            "frac": ipc / 4.0, "warp_inst_per_launch": inst,
+            "source": "instruction count: " + cap.get("source", "profiles/render_traffic.json")
+                      + "; time: live CUDA events of this run; clock: nvidia-smi median during the run"}
 
 
 def cpu_baseline(scene, cams, sample_stride: int = 1):
@@ -298,6 +319,11 @@ def main():
                 "algorithmic_bytes_per_launch": bytes_per_launch,
                 "bytes_model": "160 B per evaluated sample with alpha > 0, 20 B per density-only "
                                "sample (SURVEY 8(d)); launch = one chunk of 16 views",
+                "l2_bytes_per_launch": _ncu_capture().get("l2_bytes_per_launch"),
+                "note": "algorithmic gather bytes over the live launch time; texels are served from "
+                        "L1 (86 % hit) and L2, DRAM traffic (`traffic`) is ~5 % of the algorithmic "
+                        "bytes, so frac can exceed 1: the kernel is instruction-issue bound "
+                        "(roofline_issue)",
                 "pipeline_ms_per_step": {"setup": kt["setup_ms"] / args.steps,
                                          "march": kt["march_ms"] / args.steps,
                                          "shade": kt["shade_ms"] / args.steps,
@@ -358,6 +384,8 @@ def main():
             "mean_segments_per_ray": n_seg / n_ray_timed,
             "gather_gbs": achieved,
             "roofline": roofline,
+            "roofline_issue": issue_roofline(roofline["avg_launch_ms"], (clk or {}).get("sm_mhz") or 0,
+                                             torch.cuda.get_device_properties(local).multi_processor_count),
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": kt["setup_launches"] + kt["march_launches"] + kt["shade_launches"],

@@ -17,7 +17,8 @@ def main():
     ap.add_argument("--kernel", default="march_kernel", help="kernel-name regex (report may hold several)")
     a = ap.parse_args()
     out = subprocess.run(["ncu", "-i", a.report, "-k", "regex:" + a.kernel, "--page", "raw", "--csv", "--print-units", "base", "--metrics",
-                          "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum"],
+                          "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,smsp__inst_executed.sum,"
+                          "lts__t_sectors.sum,sm__cycles_elapsed.avg"],
                          capture_output=True, text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr = rows[0]
@@ -28,6 +29,9 @@ def main():
                    " one launch = 16 views at 1080p, tools/prof_render.py --views 16)",
          "dram_bytes_read_per_launch": rd, "dram_bytes_write_per_launch": wr, "dram_bytes_per_launch": rd + wr,
          "ncu_duration_ns": float(r["gpu__time_duration.sum"]),
+         "warp_inst_per_launch": float(r["smsp__inst_executed.sum"]),
+         "l2_bytes_per_launch": 32.0 * float(r["lts__t_sectors.sum"]),
+         "sm_cycles_per_launch": float(r["sm__cycles_elapsed.avg"]),
          "note": "includes the workspace (segments read, accumulators written); scene texels hit L1/L2"}
     with open(a.out, "w") as f:
         json.dump(d, f, indent=1)
