@@ -54,7 +54,13 @@ template <int KF> struct Geo {
 };
 
 constexpr int kSetupThreads = 128;
-constexpr int kMarchThreads = 256;
+// March CTA shape: 128 threads, 9 resident CTAs/SM (56 registers, 36 warps/SM) measured
+// +0.9 % over 256 x 4 (64 registers, 32 warps); 128 x 10 (48 registers) spills and is -7 %.
+#ifndef MERF_MARCH_THREADS
+#define MERF_MARCH_THREADS 128
+#define MERF_MARCH_MINB 9
+#endif
+constexpr int kMarchThreads = MERF_MARCH_THREADS;
 // March scheduling policy, tuned on B200 (bench workload sweeps): a warp takes a new tile of
 // 32 rays only when all its lanes are idle (per-lane refill broke the tile coherence the
 // skipping relies on and was 1.5-2x slower).  A round = one traversal step of every lane
@@ -446,7 +452,7 @@ __device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, i
 // the next occupied sample, crossing segments, finishing/refilling rays) with a converged
 // shading step.
 template <int KF>
-__global__ void __launch_bounds__(kMarchThreads, 4) march_kernel(DevScene S, int64_t n_rays, Workspace ws,
+__global__ void __launch_bounds__(kMarchThreads, MERF_MARCH_MINB) march_kernel(DevScene S, int64_t n_rays, Workspace ws,
                                                               uint32_t rflags, TraceArgs ta,
                                                               unsigned long long* stats, MarchTune tune) {
     const unsigned FULL = 0xffffffffu;

@@ -110,9 +110,9 @@ def test_null_arguments_rejected(M):
 
 
 def test_ptxas_has_no_spills(M):
-    """the production kernels stay (essentially) in registers: shade none, the timed march
-    variant at most one spilled register (it runs at the 64-register cap that gives 4
-    CTAs/SM, measured faster than 80 registers / 3 CTAs), debug/counter variants a few more;
+    """the production kernels stay in registers: shade none, the march variants none at the
+    56-register cap that gives 9 CTAs of 128 threads per SM (measured fastest), the trace /
+    counter variants a few spilled registers;
     the fp64 setup kernel may save a few bytes around the IEEE division slow-path call (the
     production variant <0> none; the per-ray trace variant <1> a few more)."""
     import sys
@@ -123,10 +123,12 @@ def test_ptxas_has_no_spills(M):
     for k, v in info.items():
         if k.startswith("shade_kernel") or k.startswith("shade_mma_kernel"):
             assert v["spill_st"] == 0 and v["spill_ld"] == 0 and v["stack"] == 0, (k, v)
-        elif k in ("march_kernel<0>", "march_kernel<16>"):
-            assert v["spill_st"] <= 8 and v["regs"] <= 64, (k, v)
-        elif k.startswith("march_kernel"):
-            assert v["spill_st"] <= 64, (k, v)
+        elif k.startswith("march_kernel<"):
+            kf = int(k[len("march_kernel<"):-1])
+            if kf & 3:      # KF_TRACE / KF_COUNT diagnostics: a few spilled registers allowed
+                assert v["spill_st"] <= 128, (k, v)
+            else:           # production variants: registers only, at the 9-CTA/SM cap
+                assert v["spill_st"] == 0 and v["stack"] == 0 and v["regs"] <= 56, (k, v)
         elif k == "setup_kernel<0>":
             assert v["spill_st"] == 0 and v["stack"] == 0, (k, v)
         elif k.startswith("setup_kernel"):
