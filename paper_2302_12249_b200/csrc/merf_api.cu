@@ -76,6 +76,12 @@ extern "C" int32_t merf_version(void) { return 100; }
 
 // keep call workspaces cached in the device's stream-ordered pool between calls (no
 // re-mapping of pages per call)
+static int current_device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d;
+}
+
 static void keep_pool_cached(int device) {
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
@@ -800,6 +806,7 @@ extern "C" merf_status merf_build_occupancy(const uint32_t* finest_bits, const m
     if (e) return e;
     if (!finest_bits || (!levels_out && desc->n_levels > 1)) return fail(MERF_EINVAL, "NULL argument");
     const int nl = desc->n_levels;
+    keep_pool_cached(current_device());   // stream-ordered temporaries of the halving chain
     // offsets of the coarser levels in levels_out (coarse -> fine), built fine -> coarse, each
     // from the next finer one (levels are nested: each divides the next)
     int64_t off[MERF_MAX_LEVELS] = {0, 0, 0, 0};
@@ -827,16 +834,19 @@ extern "C" merf_status merf_build_block_index(const uint32_t* finest_bits, const
     void* d_tmp = nullptr;
     size_t tb = 0;
     CUDA_TRY(launch_block_number(nullptr, slots, nullptr, nullptr, nullptr, &tb, nullptr, st));
-    CUDA_TRY(cudaMalloc(&d_need, slots));
-    CUDA_TRY(cudaMalloc(&d_scan, slots * 8));
-    CUDA_TRY(cudaMalloc(&d_count, 16));
-    CUDA_TRY(cudaMalloc(&d_tmp, tb + 16));
+    // stream-ordered temporaries from the (cached) default pool: no device-wide
+    // cudaMalloc/cudaFree synchronisation per call
+    keep_pool_cached(current_device());
+    CUDA_TRY(cudaMallocAsync(&d_need, slots, st));
+    CUDA_TRY(cudaMallocAsync(&d_scan, slots * 8, st));
+    CUDA_TRY(cudaMallocAsync(&d_count, 16, st));
+    CUDA_TRY(cudaMallocAsync(&d_tmp, tb + 16, st));
     CUDA_TRY(launch_block_need(finest_bits, Nf, desc->L, d_need, st));
     CUDA_TRY(launch_block_number(d_need, slots, index_out, d_count, d_tmp, &tb, d_scan, st));
     int64_t cnt = 0;
     CUDA_TRY(cudaMemcpyAsync(&cnt, d_count, 8, cudaMemcpyDeviceToHost, st));
+    cudaFreeAsync(d_need, st); cudaFreeAsync(d_scan, st); cudaFreeAsync(d_count, st); cudaFreeAsync(d_tmp, st);
     CUDA_TRY(cudaStreamSynchronize(st));
-    cudaFree(d_need); cudaFree(d_scan); cudaFree(d_count); cudaFree(d_tmp);
     *n_blocks = cnt;
     return MERF_OK;
 }
