@@ -5,17 +5,17 @@
 //     pixel tiles): raygen -> region segmentation of the world ray into <= 7 contracted
 //     segments -> per segment the int32 lattice origin Qa, step U and sample
 //     count K -> workspace (32 B per segment).
-//  2. march_kernel (int32 lattice + fp32 shading; persistent warps with ray refill):
-//     Q_k = Qa + k U; coarse-to-fine occupancy probes; an empty cell jumps to the first
-//     lattice sample outside it (the ray-AABB exit).  An evaluated sample reads the
-//     DENSITY first -- one 8-byte octet of the block-sparse grid (through the indirection
-//     table) + one 4-byte quad per plane, i.e. 4 loads for the 8 trilinear + 12 bilinear
-//     corners (Eq. 5) -- computes alpha = 1 - exp(-tau Delta) and reads the appearance
-//     texels only if alpha > alpha_skip; composite (Eq. 1-2) with termination at
-//     T < 2e-4.  Lanes whose ray ended take the next ray of the warp's tile pool, so
-//     the shading code runs with (nearly) full warps regardless of ray-length variance.
-//  3. shade_kernel (coherent tiles): deferred MLP h(C_d, F, d) per pixel (Eq. 3),
-//     C = clamp(C_d + h), store RGB f32 or RGBA8.
+//  2. march_kernel (int32 lattice + fp32 shading; persistent warps, one coherent 8x4 tile
+//     of rays per warp): Q_k = Qa + k U; one occupancy probe per step (the dyadic skip
+//     table, or the scene's levels finest-first); an empty cell jumps to the first lattice
+//     sample outside it (the ray-AABB exit).  An evaluated sample reads the DENSITY
+//     first -- one 8-byte octet of the block-sparse grid (through the indirection table) +
+//     one 4-byte quad per plane, i.e. 4 loads for the 8 trilinear + 12 bilinear corners
+//     (Eq. 5) -- computes alpha = 1 - exp(-tau Delta) and reads the appearance texels only
+//     if alpha > alpha_skip; composite (Eq. 1-2) with termination at T < 2e-4
+//     (P:309).  A warp takes its next tile when all 32 of its rays have ended.
+//  3. shade_mma_kernel (merf_shade_mma.cu, tensor cores) or shade_kernel (FFMA): deferred
+//     MLP h(C_d, F, d) per pixel (Eq. 3), C = clamp(C_d + h), store RGB f32 / RGBA8.
 #pragma once
 #include <cstdint>
 #include <climits>
@@ -446,11 +446,11 @@ __device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, i
     return ret;
 }
 
-// Persistent march.  Every lane owns one ray at a time; a warp takes tiles of 32 rays from
-// the global queue and hands them to idle lanes, so warps stay full while rays of very
-// different lengths finish.  The loop alternates a divergent traversal step (advance to
-// the next occupied sample, crossing segments, finishing/refilling rays) with a converged
-// shading step.
+// Persistent march.  Every lane owns one ray at a time; a warp takes the next tile of 32
+// coherent rays from the global queue once all its lanes are idle (refilling single lanes or
+// half tiles breaks the coherence the skipping relies on: measured 1.5-2x and 1.27x slower).
+// Each round is one traversal step of every lane holding a ray (segment transition, probe,
+// skip or find) followed by the shading of the lanes that found a sample.
 template <int KF>
 __global__ void __launch_bounds__(kMarchThreads, MERF_MARCH_MINB) march_kernel(DevScene S, int64_t n_rays, Workspace ws,
                                                               uint32_t rflags, TraceArgs ta,
