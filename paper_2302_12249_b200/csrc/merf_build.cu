@@ -352,7 +352,11 @@ struct LevelSet {
 
 // The table is BORDERED: (N + 2)^3 entries, entry (x + 1, y + 1, z + 1) for cell (x, y, z) and
 // a one-cell border that repeats the clamped edge cell, so the march indexes it with the
-// unclamped cell Qb >> s_fin (lattice drift never leaves the cube by a whole finest cell).
+// unclamped cell Qb >> s_fin.  Lattice drift never leaves the cube by a whole finest cell:
+// sample k of a segment is within 0.5 + 0.5 k lattice units of its exact position (rounded
+// Qa and U), the exact positions lie in [-2, 2]^3, and k < K <= 4 sqrt(3) / Delta <= 3.7e6
+// for the smallest accepted Delta = 2^-19 -- below the finest cell of 2^21 units at the
+// largest table resolution N = 512 (2^22 at N = 256).
 __global__ void skiptab_kernel(LevelSet ls, uint32_t* __restrict__ tab) {
     const int nl = ls.n;
     const int N = 1 << (nl - 1);
