@@ -565,7 +565,7 @@ static merf_status render_frames(const merf_scene* s, const merf_camera* cams, i
         Wl = (W - prog->ox + prog->stride - 1) / prog->stride;
         Hl = (H - prog->oy + prog->stride - 1) / prog->stride;
     }
-    set_tiles(rs, (Wl + 7) / 8, ((Wl + 7) / 8) * ((Hl + 3) / 4));
+    set_tiles(rs, (Wl + kTileW - 1) / kTileW, ((Wl + kTileW - 1) / kTileW) * ((Hl + kTileH - 1) / kTileH));
     const int64_t rays_per_view = (int64_t)rs.tiles_per_view * 32;
     const int cv = chunk_views();
     int vpc = (int)(kChunkRays * cv / kViewsPerChunk / rays_per_view);
@@ -894,7 +894,7 @@ extern "C" merf_status merf_qat_step(const merf_qat_desc* d, const float* theta_
     RaySource rs{};
     rs.W = W;
     rs.H = H;
-    set_tiles(rs, (W + 7) / 8, ((W + 7) / 8) * ((H + 3) / 4));
+    set_tiles(rs, (W + kTileW - 1) / kTileW, ((W + kTileW - 1) / kTileW) * ((H + kTileH - 1) / kTileH));
     rs.n = (int64_t)rs.tiles_per_view * 32 * n_cams;
     if (rs.n * d->max_samples > (int64_t(1) << 31)) return fail(MERF_EINVAL, "n_rays * max_samples > 2^31");
     rs.cb.n = n_cams;
