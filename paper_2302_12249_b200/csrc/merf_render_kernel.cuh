@@ -517,9 +517,9 @@ __global__ void __launch_bounds__(kMarchThreads, MERF_MARCH_MINB) march_kernel(D
         }
 
         // ---------------- traversal: advance lanes towards their next evaluated sample ----
-        // Warp-synchronous steps; the loop ends as soon as enough lanes hold a sample to shade
-        // (lanes in long empty stretches keep skipping in the next round), so one lane's long
-        // skip chain never idles the rest of the warp.
+        // One step per lane per round by default (MarchTune: further warp-synchronous steps
+        // while fewer than shade_min lanes are ready); lanes in long empty stretches keep
+        // skipping in the next rounds, so one lane's skip chain never idles the warp.
         bool found = false;
         int Qx = 0, Qy = 0, Qz = 0, fcell = 0;
         // one traversal step of a lane that wants a sample
