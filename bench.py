@@ -259,19 +259,24 @@ def main():
             n_seg += st["segments"]
     rays_per_step = V * W_IMG * H_IMG
 
+    gathered = [torch.cuda.Event() for _ in range(2)]   # buffer b's last gather finished
+
     def step(s):
-        buf = frames[s & 1]
+        b = s & 1
+        buf = frames[b]
         with torch.cuda.stream(stream):
-            if world > 1:
-                stream.wait_stream(gstream)          # buffer reuse after its gather
+            if world > 1 and s >= 2:
+                stream.wait_event(gathered[b])       # reuse buffer b only after ITS gather (step s-2)
             ev0[s].record(stream)
             M.merf_render(scene.handle, batches[s], W_IMG, H_IMG, buf, fmt=M.MERF_RGBA_U8,
                           flags=(M.MERF_TIMED if s >= args.warmup else 0) | extra_flags, stream=stream)
             ev1[s].record(stream)
         if world > 1:
+            # the gather of step s overlaps the render of step s+1 (the other buffer)
             gstream.wait_stream(stream)
             with torch.cuda.stream(gstream):
                 gather_frames(buf, rank, world)
+                gathered[b].record(gstream)
 
     ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(steps_total)]
     ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(steps_total)]
