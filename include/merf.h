@@ -194,6 +194,22 @@ merf_status merf_render(const merf_scene *scene, const merf_camera *cams, int32_
 merf_status merf_kernel_times_get(merf_scene *scene, merf_kernel_times *out, int32_t reset);
 
 /*
+ * Single-frame sharding for multi-GPU rendering ("image tiles of 64x64
+ * interleaved by rank, to balance the uneven samples/ray"): renders exactly the pixels of the
+ * 64x64-pixel blocks b (row-major over the frame, b = bx + by * ceil(W / 64)) with
+ * b % part_count == part_rank, of every view, each with the same arithmetic as merf_render,
+ * into the full-resolution `out` (layout as merf_render); all other pixels are left
+ * untouched.  The part_count shards of one frame therefore write disjoint pixel sets whose
+ * union is the whole frame: zero-filled RGBA8 shards combine by a byte-wise sum (e.g. an
+ * NCCL reduce to the root).  part_count = 1 is merf_render.  MERF_COUNTERS is ignored.
+ * Asynchronous.  Errors: those of merf_render, MERF_EINVAL (part_count < 1 or part_rank not
+ * in [0, part_count)).
+ */
+merf_status merf_render_shard(const merf_scene *scene, const merf_camera *cams, int32_t n_cams,
+                              int32_t W, int32_t H, int32_t part_rank, int32_t part_count,
+                              int32_t format, void *out, uint32_t flags, void *stream);
+
+/*
  * Progressive rendering ("the image is first rendered at a
  * lower resolution ... additional low resolution images are rendered that are dynamically
  * combined into the final high resolution image"): pass p in [0, stride^2) renders exactly

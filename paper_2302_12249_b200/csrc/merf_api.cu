@@ -548,10 +548,14 @@ struct Progressive {
     int stride, ox, oy, fill;
 };
 
+struct Shard {
+    int rank, count;
+};
+
 static merf_status render_frames(const merf_scene* s, const merf_camera* cams, int32_t n_cams,
                                  int32_t W, int32_t H, int32_t format, void* out, uint32_t flags,
                                  cudaStream_t st, unsigned long long* d_stats,
-                                 const Progressive* prog = nullptr) {
+                                 const Progressive* prog = nullptr, const Shard* shard = nullptr) {
     const size_t px_bytes = format == MERF_RGBA_U8 ? 4 : 12;
     RaySource rs{};
     rs.W = W;
@@ -566,6 +570,14 @@ static merf_status render_frames(const merf_scene* s, const merf_camera* cams, i
         Hl = (H - prog->oy + prog->stride - 1) / prog->stride;
     }
     set_tiles(rs, (Wl + kTileW - 1) / kTileW, ((Wl + kTileW - 1) / kTileW) * ((Hl + kTileH - 1) / kTileH));
+    if (shard && shard->count > 1) {       // 64x64 blocks interleaved by rank
+        rs.part_n = shard->count;
+        rs.part_r = shard->rank;
+        rs.nbx = (W + 63) / 64;
+        rs.n_pblocks = rs.nbx * ((H + 63) / 64);
+        const int slots = (rs.n_pblocks + shard->count - 1) / shard->count;
+        set_tiles(rs, rs.tiles_x, slots * kShardTiles);
+    }
     const int64_t rays_per_view = (int64_t)rs.tiles_per_view * 32;
     const int cv = chunk_views();
     int vpc = (int)(kChunkRays * cv / kViewsPerChunk / rays_per_view);
@@ -613,6 +625,18 @@ extern "C" merf_status merf_render(const merf_scene* s, const merf_camera* cams,
         if (stats) to_stats(h, stats);
     }
     return MERF_OK;
+}
+
+extern "C" merf_status merf_render_shard(const merf_scene* s, const merf_camera* cams, int32_t n_cams,
+                                         int32_t W, int32_t H, int32_t part_rank, int32_t part_count,
+                                         int32_t format, void* out, uint32_t flags, void* stream) {
+    merf_status e = check_frames(s, cams, n_cams, W, H, format, out);
+    if (e) return e;
+    if (part_count < 1 || part_rank < 0 || part_rank >= part_count)
+        return fail(MERF_EINVAL, "need 0 <= part_rank < part_count (got %d of %d)", part_rank, part_count);
+    Shard sh{part_rank, part_count};
+    return render_frames(s, cams, n_cams, W, H, format, out, flags & ~(uint32_t)MERF_COUNTERS,
+                         (cudaStream_t)stream, nullptr, nullptr, &sh);
 }
 
 extern "C" merf_status merf_render_progressive(const merf_scene* s, const merf_camera* cams, int32_t n_cams,

@@ -99,7 +99,13 @@ struct RaySource {
     // exact division by tiles_per_view / tiles_x as a 64-bit multiply-high: m = ceil(2^64 / d)
     // gives floor(n / d) = umulhi(n, m) for all n, d < 2^32 (d >= 2); 0 = not set (divide)
     uint64_t m_tpv, m_tx;
+    // single-frame sharding (merf_render_shard): part_n > 1 -> the rays cover only the
+    // 64x64-pixel blocks b with b % part_n == part_r; a view's tile range is then part_slots
+    // block slots of kShardTiles tiles (block b = part_r + part_n * slot, row-major over the
+    // frame's nbx blocks per row, n_pblocks in total; slots past the last block are empty)
+    int part_n, part_r, nbx, n_pblocks;
 };
+constexpr int kShardBX = 64 / kTileW, kShardBY = 64 / kTileH, kShardTiles = kShardBX * kShardBY;
 
 // host: the tile geometry of a camera chunk and its division magics
 inline void set_tiles(RaySource& rs, int tiles_x, int tiles_per_view) {
@@ -125,7 +131,18 @@ __device__ __forceinline__ bool ray_pixel(const RaySource& rs, int64_t ray, int&
         view = (int)(tile / rs.tiles_per_view);
         tt = (int)(tile - (int64_t)view * rs.tiles_per_view);
     }
-    const int ty = (int)div_magic((unsigned)tt, (unsigned)rs.tiles_x, rs.m_tx), tx = tt - ty * rs.tiles_x;
+    int ty, tx;
+    if (rs.part_n > 1) {
+        const int slot = tt / kShardTiles, w = tt - slot * kShardTiles;
+        const int b = rs.part_r + rs.part_n * slot;
+        if (b >= rs.n_pblocks) return false;          // padding slot of this shard
+        const int by = b / rs.nbx, bx = b - by * rs.nbx;
+        tx = bx * kShardBX + (w % kShardBX);
+        ty = by * kShardBY + (w / kShardBX);
+    } else {
+        ty = (int)div_magic((unsigned)tt, (unsigned)rs.tiles_x, rs.m_tx);
+        tx = tt - ty * rs.tiles_x;
+    }
     const int lx = tx * kTileW + (lane % kTileW), ly = ty * kTileH + (lane / kTileW);
     px = lx * rs.stride_m1 + lx + rs.ox;
     py = ly * rs.stride_m1 + ly + rs.oy;

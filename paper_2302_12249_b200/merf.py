@@ -93,6 +93,8 @@ SIGNATURES = [
                               C.POINTER(merf_stats)]),
     ("merf_render_progressive", C.c_int, [_vp, C.POINTER(merf_camera), _i32, _i32, _i32, _i32, _i32, _i32, _i32,
                                           _vp, _u32, _vp]),
+    ("merf_render_shard", C.c_int, [_vp, C.POINTER(merf_camera), _i32, _i32, _i32, _i32, _i32, _i32, _vp, _u32,
+                                    _vp]),
     ("merf_render_host", C.c_int, [_vp, C.POINTER(merf_camera), _i32, _i32, _i32, _i32, _vp, _u32, _vp]),
     ("merf_render_rays", C.c_int, [_vp, _vp, _vp, _vp, _i64, _vp, _u32, _vp, C.POINTER(merf_stats)]),
     ("merf_trace", C.c_int, [_vp, C.POINTER(merf_camera), _i32, _vp, _i64, _i32, _vp, _vp, _vp, _u32,
@@ -244,6 +246,23 @@ def merf_render_progressive(handle, cams, W: int, H: int, stride: int, pass_: in
     carr = cameras_to_c(cams)
     _check(lib().merf_render_progressive(handle, carr, len(carr), int(W), int(H), int(stride), int(pass_),
                                          int(bool(fill)), int(fmt), _ptr(out), int(flags), _stream(stream)))
+
+
+def shard_owner(W: int, H: int, part_count: int):
+    """Owner rank of every pixel under merf_render_shard's partition (host-side indexing, for
+    assembling / checking sharded frames): 64x64 blocks, row-major, block b -> rank b % N."""
+    by = np.arange(H)[:, None] // 64
+    bx = np.arange(W)[None, :] // 64
+    return ((by * ((W + 63) // 64) + bx) % part_count).astype(np.int32)
+
+
+def merf_render_shard(handle, cams, W: int, H: int, part_rank: int, part_count: int, out,
+                      fmt: int = MERF_RGB_F32, flags: int = 0, stream=None) -> None:
+    """Render the 64x64-pixel blocks b with b % part_count == part_rank of every view into the
+    full-size `out` (SURVEY 8(e) single-frame sharding); other pixels are left untouched."""
+    carr = cameras_to_c(cams)
+    _check(lib().merf_render_shard(handle, carr, len(carr), int(W), int(H), int(part_rank), int(part_count),
+                                   int(fmt), _ptr(out), int(flags), _stream(stream)))
 
 
 def merf_render_host(handle, cams, W: int, H: int, out_host, fmt: int = MERF_RGBA_U8,

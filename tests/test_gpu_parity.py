@@ -587,3 +587,34 @@ def test_mlp_mma_rays_and_u8(M, c1_scene):
     f32, _ = _gpu_frame(M, c1_scene, cams, W, H)
     u8, _ = _gpu_frame(M, c1_scene, cams, W, H, fmt=M.MERF_RGBA_U8)
     assert np.array_equal(u8[..., :3], np.rint(f32 * 255).astype(np.uint8))
+
+
+# ------------------------------------------------------------------------------------
+# single-frame sharding (merf_render_shard): 64x64 blocks interleaved by rank
+# ------------------------------------------------------------------------------------
+@pytest.mark.parametrize("N,WH", [(2, (1920, 1080)), (3, (130, 70)), (5, (257, 129)), (1, (64, 64))])
+def test_render_shard_partition(M, c1_scene, c2, N, WH):
+    import torch
+    W, H = WH
+    sc = c2 if W >= 1000 else c1_scene
+    cam = orbit_cameras(256, indices=[9], W=W, H=H) if W >= 1000 else \
+        look_at_camera(np.array([0.1, 0.05, -0.2]), target=np.zeros(3), W=W, H=H, fov_x_deg=60)[None]
+    s = M.Scene(sc)
+    full = torch.zeros((1, H, W, 4), dtype=torch.uint8, device="cuda")
+    M.merf_render(s.handle, cam, W, H, full, fmt=M.MERF_RGBA_U8)
+    acc = torch.zeros((1, H, W, 4), dtype=torch.int32, device="cuda")
+    owner = M.shard_owner(W, H, N)
+    for r in range(N):
+        part = torch.zeros((1, H, W, 4), dtype=torch.uint8, device="cuda")
+        M.merf_render_shard(s.handle, cam, W, H, r, N, part, fmt=M.MERF_RGBA_U8)
+        torch.cuda.synchronize()
+        p = part.cpu().numpy()[0]
+        # the shard writes exactly its own blocks (alpha 255 there, untouched zeros elsewhere)
+        assert np.array_equal(p[..., 3] == 255, owner == r)
+        acc += part.to(torch.int32)
+    torch.cuda.synchronize()
+    # disjoint shards sum (e.g. an NCCL reduce) to the unsharded frame, byte for byte
+    assert np.array_equal(acc.cpu().numpy().astype(np.uint8), full.cpu().numpy())
+    with pytest.raises(M.MerfError):
+        M.merf_render_shard(s.handle, cam, W, H, N, N, full, fmt=M.MERF_RGBA_U8)
+    s.close()
