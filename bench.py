@@ -247,6 +247,7 @@ def main():
 
     # ---- counters pass over exactly the launches timed below (untimed, same views)
     algo_bytes, n_eval, n_donly, n_skip, n_seg = [], 0, 0, 0, 0
+    region_segs = [0] * 7
     with torch.cuda.stream(stream):
         for s in range(args.warmup, steps_total):
             st = M.merf_render(scene.handle, batches[s], W_IMG, H_IMG, frames[0], fmt=M.MERF_RGBA_U8,
@@ -257,6 +258,7 @@ def main():
             n_donly += st["density_only"]
             n_skip += st["skips"]
             n_seg += st["segments"]
+            region_segs = [a + b for a, b in zip(region_segs, st["region_segments"])]
     rays_per_step = V * W_IMG * H_IMG
 
     gathered = [torch.cuda.Event() for _ in range(2)]   # buffer b's last gather finished
@@ -302,10 +304,13 @@ def main():
     ms = t_start.elapsed_time(t_end)
     call_ms = [ev0[s].elapsed_time(ev1[s]) for s in range(args.warmup, steps_total)]
     kt = M.merf_kernel_times_get(scene.handle, reset=True)
+    rank_ms = [ms]
     if world > 1:
         t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        allt = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(allt, t)                      # per-rank times: imbalance
+        rank_ms = [float(x.item()) for x in allt]
+        ms = max(rank_ms)
     ms_per_step = ms / args.steps
     total_rays = rays_per_step * world * args.steps
     value = total_rays / (ms / 1e3)
@@ -387,6 +392,9 @@ def main():
             "density_only_fraction": n_donly / max(n_eval, 1),
             "mean_skips_per_ray": n_skip / n_ray_timed,
             "mean_segments_per_ray": n_seg / n_ray_timed,
+            "segments_per_region": dict(zip(["core", "+x", "-x", "+y", "-y", "+z", "-z"], region_segs)),
+            "rank_ms": rank_ms,
+            "rank_imbalance": max(rank_ms) / (sum(rank_ms) / len(rank_ms)),
             "gather_gbs": achieved,
             "roofline": roofline,
             "roofline_issue": issue_roofline(roofline["avg_launch_ms"], (clk or {}).get("sm_mhz") or 0,
