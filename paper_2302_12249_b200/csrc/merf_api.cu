@@ -230,6 +230,7 @@ extern "C" merf_status merf_scene_upload(const merf_scene_desc* desc, const uint
     s->desc = *desc;
     s->device = device;
     s->n_blocks = use_v ? n_blocks : 0;
+    s->dev.n_blocks_dev = (int)s->n_blocks;
     fill_dev(s);
     DevScene& S = s->dev;
     auto bail = [&](merf_status e) { merf_scene_free(s); cudaSetDevice(prev); return e; };

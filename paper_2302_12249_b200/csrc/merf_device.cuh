@@ -45,6 +45,7 @@ struct DevScene {
     // per-lane mma fragments of the MLP (merf_shade_mma.cu); NULL = FFMA shade kernel
     const uint32_t* mlp_frag;     // [32][kMlpFragWords]
     int L, R, nb, n_levels;
+    int n_blocks_dev;             // atlas blocks (bounds checks of MERF_BOUNDS_CHECK builds)
     int level_res[MERF_MAX_LEVELS];
     int level_shift[MERF_MAX_LEVELS];   // F + 2 - log2(N)
     int sV, sP;                   // F + 2 - log2(L), F + 2 - log2(R)
@@ -296,6 +297,14 @@ __device__ __forceinline__ void texel(int Qb, int s, int M, int& i0, float& f) {
 // The same texel coordinate with the fraction delivered as g = 2^23 + f 2^s, an exact float
 // built by one LOP3 (needs s <= 23; the compile-time paper geometry has s = 21, 19): no I2F and
 // no scaling multiply.  g_frac recovers f exactly (power-of-two scaling, one FFMA).
+// MERF_BOUNDS_CHECK builds (tests / stress only): every gathered index is checked against its
+// buffer and a violation traps (compute-sanitizer is unavailable on the GPU pool)
+#ifdef MERF_BOUNDS_CHECK
+#define MERF_CHECK(cond) do { if (!(cond)) __trap(); } while (0)
+#else
+#define MERF_CHECK(cond) do { } while (0)
+#endif
+
 __device__ __forceinline__ float exp2i(int n) { return __int_as_float((127 + n) << 23); }
 __device__ __forceinline__ void texel_g(int Qb, int s, int M, int& i0, float& g) {
     const int P = min(max(Qb - (1 << (s - 1)), 0), (M - 1) << s);

@@ -351,8 +351,10 @@ __device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, i
         const int nb = Geo<KF>::nb(S);
         const int slot = ((vi[2] >> 3) * nb + (vi[1] >> 3)) * nb + (vi[0] >> 3);
         if (slot != bslot) {                              // blocks change every ~8 voxels
+            MERF_CHECK(slot >= 0 && slot < nb * nb * nb);
             bslot = slot;
             bblk = __ldg(S.block_index + slot);
+            MERF_CHECK(bblk < S.n_blocks_dev);
         }
         blk = bblk;
         uint32_t zi[2], yi[4];
@@ -382,6 +384,7 @@ __device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, i
         }
         if (ALL || blk >= 0) {
             // ---- density pass, V: the corner octet (byte c = dx + 2 dy + 4 dz) as 4 dp2a
+            MERF_CHECK(blk >= 0 && blk < max(S.n_blocks_dev, 1));
             const uint2 oct = __ldg(S.vdens + (unsigned)(blk * 512 + ((vi[2] & 7) * 8 + (vi[1] & 7)) * 8 + (vi[0] & 7)));
             sd = __dp2a_lo(wV[0], oct.x, sd);
             sd = __dp2a_hi(wV[1], oct.x, sd);
@@ -421,6 +424,7 @@ __device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, i
             wP[a][0] = wleaf(v0i, v0f, pf[ua]);
             wP[a][1] = wleaf(v1i, v1f, pf[ua]);
             // ---- density pass, plane a: the texel quad (byte du + 2 dv) as 2 dp2a
+            MERF_CHECK(pi[va] >= 0 && pi[va] < R && pi[ua] >= 0 && pi[ua] < R);
             const uint32_t quad = __ldg(S.pdens + plane_index<KF>(a, R, pi[va], pi[ua]));
             sd = __dp2a_lo(wP[a][0], quad, sd);
             sd = __dp2a_hi(wP[a][1], quad, sd);
@@ -560,6 +564,7 @@ __global__ void __launch_bounds__(kMarchThreads, MERF_MARCH_MINB) march_kernel(D
                 fcell = ((Qz >> sf) * Nb + (Qy >> sf)) * Nb + (Qx >> sf) + (Nb * Nb + Nb + 1);
                 if (fcell == last_cell) { found = true; return; }  // same finest cell: all levels set
                 // one probe: 0 = occupied, else the shift of the coarsest empty level - 16
+                MERF_CHECK(fcell >= 0 && (int64_t)fcell < (int64_t)Nb * Nb * Nb);
                 const unsigned code = __ldg(reinterpret_cast<const uint8_t*>(S.skiptab) + (unsigned)fcell);
                 if (code == 0u) { found = true; return; }
                 const int sh = (int)code + 16;
