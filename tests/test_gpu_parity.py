@@ -618,3 +618,16 @@ def test_render_shard_partition(M, c1_scene, c2, N, WH):
     with pytest.raises(M.MerfError):
         M.merf_render_shard(s.handle, cam, W, H, N, N, full, fmt=M.MERF_RGBA_U8)
     s.close()
+
+
+def test_randomised_stress_one_case_per_geometry(M):
+    """tools/stress_parity.py, one random case per geometry (paper geometry, small grids,
+    V-only, planes-only, V + one plane): every pixel within 2e-3 of the oracle, every pixel's
+    trace (termination off) bit-exact."""
+    import importlib.util
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("stress_parity", os.path.join(root, "tools", "stress_parity.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    assert mod.run(len(mod.GEOMS), seed=2026, verbose=False) == 0

@@ -28,22 +28,19 @@ GEOMS = [  # (L, R, level_res, step, source_mask, occ_fraction)
 ]
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--cases", type=int, default=24)
-    ap.add_argument("--seed", type=int, default=0)
-    a = ap.parse_args()
+def run(cases: int, seed: int, verbose: bool = True) -> int:
+    """run `cases` randomised cases; returns the number of failures"""
     import torch
     from merf_inputs import random_scene, look_at_camera
     from oracle import oracle as O
     import paper_2302_12249_b200 as M
-    rng = np.random.default_rng(a.seed)
+    rng = np.random.default_rng(seed)
     bad = 0
-    for case in range(a.cases):
+    for case in range(cases):
         L, R, lv, step, mask, occ = GEOMS[case % len(GEOMS)]
-        seed = int(rng.integers(1 << 30))
+        sseed = int(rng.integers(1 << 30))
         t0 = time.time()
-        sc = random_scene(seed=seed, L=L, R=R, level_res=lv, step=step, source_mask=mask,
+        sc = random_scene(seed=sseed, L=L, R=R, level_res=lv, step=step, source_mask=mask,
                           occ_fraction=occ, density_offset=int(rng.integers(-30, 10)))
         W, H = int(rng.integers(17, 97)), int(rng.integers(9, 61))
         pos = rng.uniform(-1.2, 1.2, 3) if rng.random() < 0.5 else rng.normal(0, 4, 3)
@@ -68,12 +65,22 @@ def main():
                         and np.array_equal(cells.cpu().numpy().view(np.uint64), o["trace_cells"]))
         ok = err <= 2e-3 and trace_ok
         bad += not ok
-        print(json.dumps({"case": case, "L": L, "R": R, "levels": lv, "step": step, "mask": mask, "seed": seed,
-                          "W": W, "H": H, "cam_pos": [round(float(x), 3) for x in pos], "max_err": err,
-                          "traces_bit_exact": trace_ok, "samples": int(ref["stats"]["evaluated"]),
-                          "ok": ok, "s": round(time.time() - t0, 1)}), flush=True)
-    print(json.dumps({"cases": a.cases, "failures": bad}))
-    sys.exit(1 if bad else 0)
+        if verbose:
+            print(json.dumps({"case": case, "L": L, "R": R, "levels": lv, "step": step, "mask": mask, "seed": sseed,
+                              "W": W, "H": H, "cam_pos": [round(float(x), 3) for x in pos], "max_err": err,
+                              "traces_bit_exact": trace_ok, "samples": int(ref["stats"]["evaluated"]),
+                              "ok": ok, "s": round(time.time() - t0, 1)}), flush=True)
+    if verbose:
+        print(json.dumps({"cases": cases, "failures": bad}))
+    return bad
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--cases", type=int, default=24)
+    ap.add_argument("--seed", type=int, default=0)
+    a = ap.parse_args()
+    sys.exit(1 if run(a.cases, a.seed) else 0)
 
 
 if __name__ == "__main__":
