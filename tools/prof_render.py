@@ -1,7 +1,9 @@
-"""One warm render launch of the bench workload for ncu (--set full) captures.
+"""Warm render launches of the bench workload for ncu (--set full) captures: two warm-up
+renders, then one render with counters (its stats are printed).  Each render is one setup,
+one march and one shade launch, so `-k regex:"march_kernel|shade_mma|setup_kernel" -s 3 -c 3`
+captures the second render's three kernels (tools/gpu_profile_round.sh).
 
-  python tools/prof_render.py [--views N] [--u8]
-The profiled launch is the 2nd render_kernel launch (use ncu -k regex:render_kernel -s 1 -c 1).
+  python tools/prof_render.py [--views N] [--first K]
 """
 import argparse
 import os
