@@ -234,6 +234,8 @@ def main():
 
     sc = make_scene("c2", contraction="sph" if args.spherical else "pi")
     scene = M.Scene(sc, device=local)
+    n_fin = sc.level_res[-1]
+    occ_frac = float(np.unpackbits(sc.occ_finest.view(np.uint8)).sum()) / n_fin ** 3
     info = scene.info()
     V = args.views
     steps_total = args.warmup + args.steps
@@ -380,6 +382,7 @@ def main():
                        "views_per_rank_per_step": V, "W": W_IMG, "H": H_IMG,
                        "scene": {k: info[k] for k in ("L", "R", "level_res", "n_blocks", "device_bytes")},
                        "block_fraction": info["n_blocks"] / (info["L"] // 8) ** 3 if info["L"] else None,
+                       "finest_occupancy_fraction": occ_frac,
                        "l2": "no flush: inputs (scene %.0f MB) larger than the 126 MB L2; each step renders "
                              "different orbit views" % (info["device_bytes"] / 1e6),
                        "parallelism": f"views sharded over {world} rank(s), scene replicated, "
