@@ -261,8 +261,8 @@ merf_status merf_trace(const merf_scene *scene, const merf_camera *cam, int32_t 
                        void *stream);
 
 /* One contracted segment of a ray: world interval [t_a, t_b] (t_b = +inf for the
- * unbounded last one), region (0 core, 1 + 2j + (s < 0)), lattice origin Qa = llrint(c_a 2^40),
- * lattice step U = llrint(u Delta 2^40) and sample count K = ceil(l / Delta) (readings D5-D8). */
+ * unbounded last one), region (0 core, 1 + 2j + (s < 0)), lattice origin Qa = llrint(c_a 2^28),
+ * lattice step U = llrint(u Delta 2^28) and sample count K = ceil(l / Delta) (readings D5-D8). */
 typedef struct {
     double t_a, t_b;
     int64_t Qa[3];

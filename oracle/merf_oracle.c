@@ -286,7 +286,9 @@ void orc_maxpool_bits(const uint32_t *fine, int32_t f, uint32_t *coarse, int32_t
 /* ---------------------------------------------------------------------------------- */
 static int ilog2i(int64_t v) { int n = 0; while (((int64_t)1 << n) < v) n++; return n; }
 
-/* occupancy cell index at resolution N for lattice coordinate Q (D10) */
+/* occupancy cell index at resolution N for lattice coordinate Q (D10): the cell of
+ * [-2, 2) split into N equal half-open cells that contains Q 2^-F, clamped to [0, N-1]
+ * (pinned against real arithmetic in tests/test_oracle_lattice.py) */
 static int64_t occ_cell(int64_t Q, int32_t N)
 {
     int s = ORC_F + 2 - ilog2i(N);
@@ -295,6 +297,9 @@ static int64_t occ_cell(int64_t Q, int32_t N)
     if (c > N - 1) c = N - 1;
     return c;
 }
+
+/* exported for the pins only */
+int64_t orc_occ_cell(int64_t Q, int32_t N) { return occ_cell(Q, N); }
 
 /* lower texel index i0 and fraction f of coordinate Q on a grid of resolution M */
 static void texel_coord(int64_t Q, int32_t M, int64_t *i0, double *f)

@@ -72,6 +72,8 @@ def lib():
             L.orc_raygen.argtypes = [vp, i32, i32, vp, vp]
             L.orc_segment_ray.argtypes = [vp, vp, dbl, dbl, vp]
             L.orc_segment_ray.restype = C.c_int
+            L.orc_occ_cell.argtypes = [i64, i32]
+            L.orc_occ_cell.restype = i64
             L.orc_maxpool_bits.argtypes = [vp, i32, vp, i32]
             L.orc_canonical_block_index.argtypes = [vp, i32, i32, vp]
             L.orc_canonical_block_index.restype = i64
@@ -151,6 +153,11 @@ def segment_ray(o, d, t_near: float, step: float):
 # ------------------------------------------------------------------------------------
 # occupancy pyramid / block index
 # ------------------------------------------------------------------------------------
+def occ_cell(Q: int, N: int) -> int:
+    """occupancy cell index at resolution N of the (unbiased) lattice coordinate Q (D10)."""
+    return int(lib().orc_occ_cell(int(Q), int(N)))
+
+
 def n_words(N: int) -> int:
     return (N * N * N + 31) // 32
 

@@ -2,7 +2,7 @@
 //
 // Canonical fp64 ray setup (reading D8 in DESIGN.md): every fp64 operation that decides
 // the integer lattice (ray generation, region segmentation, contraction of segment
-// endpoints, segment length/direction, llrint to the 2^-40 lattice) uses the _rn
+// endpoints, segment length/direction, llrint to the 2^-28 lattice, F = MERF_FIXED_BITS) uses the _rn
 // intrinsics so that nvcc can never contract a multiply-add into an FMA.  The same
 // IEEE-754 operations in the same order give bit-identical lattices on any conforming
 // implementation (e.g. an fp64 CPU reference), which makes per-ray visited-cell traces
