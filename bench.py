@@ -44,7 +44,8 @@ def views_for(rank: int, world: int, step: int, per_rank: int, n_orbit: int = N_
 
 
 def gather_frames(frames, rank: int, world: int, group=None):
-    """gather every rank's frame batch to rank 0 (NCCL on GPU, gloo in tests)."""
+    """Reference semantics of the frame gather (gloo in the CPU tests): every rank's frame
+    batch to rank 0.  On the GPU bench.py gathers through libmerf's merf_gather_frames (NCCL)."""
     import torch
     import torch.distributed as dist
     if world == 1:
@@ -52,6 +53,15 @@ def gather_frames(frames, rank: int, world: int, group=None):
     out = [torch.empty_like(frames) for _ in range(world)] if rank == 0 else None
     dist.gather(frames, gather_list=out, dst=0, group=group)
     return out
+
+
+def make_comm(M, rank: int, world: int, device: int):
+    """libmerf's NCCL communicator; rank 0's unique id travels over the torch.distributed
+    store (plumbing only)."""
+    import torch.distributed as dist
+    uid = [M.merf_comm_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    return M.Comm(uid[0], world, rank, device)
 
 
 class ClockSampler:
@@ -197,6 +207,57 @@ def run_reference(args):
     return 0
 
 
+def e2e_multi(M, scene, comm, batches, args, rank, world, dev, stream, gstream, frames, root_bufs, total_rays):
+    """End to end at N > 1 through the public API, every step inside the timed region: each rank
+    renders its views (merf_render, camera parameters host -> device), the frames are gathered to
+    rank 0 (merf_gather_frames over NCCL), and rank 0 copies the gathered frames of all ranks to
+    pinned host memory.  Max over ranks."""
+    import torch
+    import torch.distributed as dist
+    V = args.views
+    host = (torch.empty((world, V, H_IMG, W_IMG, 4), dtype=torch.uint8).pin_memory() if rank == 0 else None)
+    cstream = torch.cuda.Stream()
+    ready = [torch.cuda.Event() for _ in range(2)]      # gather of buffer b done
+    copied = [torch.cuda.Event() for _ in range(2)]     # root's D2H of buffer b done
+
+    def one(s, i):
+        b = i & 1
+        if i >= 2:
+            stream.wait_event(copied[b] if rank == 0 else ready[b])
+        M.merf_render(scene.handle, batches[s], W_IMG, H_IMG, frames[b], fmt=M.MERF_RGBA_U8, stream=stream)
+        gstream.wait_stream(stream)
+        comm.gather(frames[b], root_bufs[b], root=0, stream=gstream)
+        ready[b].record(gstream)
+        if rank == 0:
+            cstream.wait_event(ready[b])
+            with torch.cuda.stream(cstream):
+                host.copy_(root_bufs[b], non_blocking=True)
+            copied[b].record(cstream)
+
+    for i, s in enumerate(range(min(2, args.warmup))):
+        one(s, i)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i, s in enumerate(range(args.warmup, args.warmup + args.steps)):
+        one(s, i)
+    stream.wait_stream(gstream)
+    stream.wait_stream(cstream)
+    e1.record(stream)
+    comm.wait(stream=stream, timeout_ms=120000)
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1)], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ems = float(t.item())
+    return {"value": total_rays / (ems / 1e3), "unit": "rays/s",
+            "h2d_bytes_per_step": world * V * 136, "d2h_bytes_per_step": world * V * W_IMG * H_IMG * 4,
+            "nccl_bytes_per_step": (world - 1) * V * W_IMG * H_IMG * 4,
+            "path": "per rank merf_render (device frames) -> merf_gather_frames to rank 0 (NCCL) -> rank 0 "
+                    "copies all ranks' frames to pinned host memory; max over ranks"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -246,6 +307,10 @@ def main():
     stream = torch.cuda.Stream()
     gstream = torch.cuda.Stream()
     frames = [torch.empty((V, H_IMG, W_IMG, 4), dtype=torch.uint8, device=dev) for _ in range(2)]
+    comm = make_comm(M, rank, world, local) if world > 1 else None
+    # the root's gather targets: [world][V][H][W][4], double buffered like the frames
+    root_bufs = ([torch.empty((world, V, H_IMG, W_IMG, 4), dtype=torch.uint8, device=dev) for _ in range(2)]
+                 if world > 1 and rank == 0 else [None, None])
 
     # ---- counters pass over exactly the launches timed below (untimed, same views)
     algo_bytes, n_eval, n_donly, n_skip, n_seg = [], 0, 0, 0, 0
@@ -276,11 +341,11 @@ def main():
                           flags=(M.MERF_TIMED if s >= args.warmup else 0) | extra_flags, stream=stream)
             ev1[s].record(stream)
         if world > 1:
-            # the gather of step s overlaps the render of step s+1 (the other buffer)
+            # the gather of step s (libmerf merf_gather_frames: grouped NCCL send/recv to rank
+            # 0) overlaps the render of step s+1 (the other buffer)
             gstream.wait_stream(stream)
-            with torch.cuda.stream(gstream):
-                gather_frames(buf, rank, world)
-                gathered[b].record(gstream)
+            comm.gather(buf, root_bufs[b], root=0, stream=gstream)
+            gathered[b].record(gstream)
 
     ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(steps_total)]
     ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(steps_total)]
@@ -303,8 +368,20 @@ def main():
     clk = clocks.stop()
     if world > 1:
         dist.barrier()
+    if comm is not None:
+        comm.wait(stream=gstream, timeout_ms=120000)  # NCCL async errors surface here
     ms = t_start.elapsed_time(t_end)
     call_ms = [ev0[s].elapsed_time(ev1[s]) for s in range(args.warmup, steps_total)]
+    gather_check = None
+    if world > 1:
+        # integrity of the last gather: rank 0's slot r holds rank r's last frames
+        last = (steps_total - 1) & 1
+        ck = torch.tensor([float(frames[last].sum(dtype=torch.int64).item())], device=dev)
+        cks = [torch.zeros_like(ck) for _ in range(world)]
+        dist.all_gather(cks, ck)
+        if rank == 0:
+            got = [float(root_bufs[last][r].sum(dtype=torch.int64).item()) for r in range(world)]
+            gather_check = all(abs(g - float(c.item())) == 0 for g, c in zip(got, cks))
     kt = M.merf_kernel_times_get(scene.handle, reset=True)
     rank_ms = [ms]
     if world > 1:
@@ -343,7 +420,10 @@ def main():
 
     # ---- end to end through the C ABI with host buffers (pinned), copies in the timed region
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and world > 1:
+        e2e = e2e_multi(M, scene, comm, batches, args, rank, world, dev, stream, gstream, frames, root_bufs,
+                        total_rays)
+    elif not args.no_e2e:
         host = torch.empty((V, H_IMG, W_IMG, 4), dtype=torch.uint8).pin_memory()
         for s in range(min(2, args.warmup)):
             M.merf_render_host(scene.handle, batches[s], W_IMG, H_IMG, host, fmt=M.MERF_RGBA_U8, stream=stream)
@@ -397,6 +477,10 @@ def main():
             "mean_segments_per_ray": n_seg / n_ray_timed,
             "segments_per_region": dict(zip(["core", "+x", "-x", "+y", "-y", "+z", "-z"], region_segs)),
             "rank_ms": rank_ms,
+            "gather": ({"path": "libmerf merf_gather_frames (grouped ncclSend/ncclRecv to rank 0 on a side "
+                                "stream, overlapped with the next step's render)",
+                        "bytes_per_step": rays_per_step * 4 * (world - 1), "verified": gather_check}
+                       if world > 1 else None),
             "rank_imbalance": max(rank_ms) / (sum(rank_ms) / len(rank_ms)),
             "gather_gbs": achieved,
             "roofline": roofline,
@@ -410,6 +494,8 @@ def main():
         }
         print(json.dumps(line), flush=True)
     scene.close()
+    if comm is not None:
+        comm.close()
     if world > 1:
         dist.destroy_process_group()
     return 0

@@ -56,7 +56,7 @@ typedef enum {
     MERF_EINVAL = 1,     /* invalid argument (null pointer, bad size, bad descriptor)     */
     MERF_ENOMEM = 2,     /* device allocation failed                                      */
     MERF_ECUDA = 3,      /* a CUDA runtime call or kernel launch failed                   */
-    MERF_ENCCL = 4,      /* reserved (frame gather is done by the caller's process group) */
+    MERF_ENCCL = 4,      /* NCCL missing, a communicator error, or a gather timeout       */
     MERF_EMISMATCH = 5,  /* scene arrays inconsistent (unsound block index, bad entries)  */
     MERF_EIO = 6         /* bundle / camera file missing, unreadable, malformed or corrupt */
 } merf_status;
@@ -208,6 +208,63 @@ merf_status merf_kernel_times_get(merf_scene *scene, merf_kernel_times *out, int
 merf_status merf_render_shard(const merf_scene *scene, const merf_camera *cams, int32_t n_cams,
                               int32_t W, int32_t H, int32_t part_rank, int32_t part_count,
                               int32_t format, void *out, uint32_t flags, void *stream);
+
+/*
+ * Compact single-frame shard: the same rays as merf_render_shard, but the output
+ * holds only this part's blocks, packed by slot: blocks_out [device] [n_cams][S][64][64] pixels
+ * (RGB f32 or RGBA8), S = merf_shard_slots(W, H, part_count), slot s = block part_rank +
+ * part_count * s (row-major blocks).  Pixels of edge blocks outside the frame and slots past
+ * the last block are not written.  This is what a rank sends to the root (merf_gather_frames);
+ * the root rebuilds the frames with merf_shard_assemble.  Asynchronous.  Errors: those of
+ * merf_render_shard.
+ */
+merf_status merf_render_shard_blocks(const merf_scene *scene, const merf_camera *cams, int32_t n_cams,
+                                     int32_t W, int32_t H, int32_t part_rank, int32_t part_count,
+                                     int32_t format, void *blocks_out, uint32_t flags, void *stream);
+
+/* Block slots per part of a W x H frame split into part_count parts (0 on bad arguments). */
+int32_t merf_shard_slots(int32_t W, int32_t H, int32_t part_count);
+
+/*
+ * Rebuild frames from the gathered compact shards: blocks [device] [part_count][n_views][S]
+ * [64][64] pixels (merf_gather_frames of every part's merf_render_shard_blocks output, part p
+ * at offset p) -> frame_out [device] [n_views][H][W] pixels (format as rendered).  Every frame
+ * pixel is written exactly once (the parts partition the blocks).  Asynchronous; one kernel.
+ * Errors: MERF_EINVAL (null, sizes, format), MERF_ECUDA.
+ */
+merf_status merf_shard_assemble(const void *blocks, int32_t n_views, int32_t W, int32_t H, int32_t part_count,
+                                int32_t format, void *frame_out, void *stream);
+
+/*
+ * Multi-GPU frame gather (the only collective of the design: rays are
+ * independent and the scene is replicated, so finished frames are the one thing exchanged;
+ * throughput context P:329).  One process per GPU.  NCCL is loaded at run time
+ * (libnccl.so.2, or the path in MERF_NCCL_LIB): without it these calls return MERF_ENCCL.
+ *
+ * merf_comm_unique_id: rank 0 creates the 128-byte id [host]; the caller distributes it to the
+ *   other ranks by any channel (e.g. a TCP store).
+ * merf_comm_init: every rank joins (blocking until all n_ranks have called it), on `device`.
+ * merf_gather_frames: rank r's `bytes` bytes at local [device] land at root_buf + r * bytes on
+ *   the root (root_buf [device], n_ranks * bytes, ignored elsewhere).  Grouped ncclSend (ranks
+ *   != root) / ncclRecv (root; its own part is a device copy), enqueued on `stream`
+ *   (asynchronous; the caller orders buffer reuse by stream events).  The communicator's async
+ *   error state (ncclCommGetAsyncError) is checked before and after enqueueing.
+ * merf_comm_wait: wait for `stream` while polling the async error state; on an error, or if
+ *   the stream has not completed after timeout_ms (< 0: no limit), the communicator is aborted
+ *   (ncclCommAbort, so the stream is released) and MERF_ENCCL returned; the communicator is then
+ *   unusable (free it).
+ * merf_comm_info: rank count, own rank and the loaded NCCL version code.
+ * Errors: MERF_EINVAL (null, rank/root out of range, device), MERF_ENCCL, MERF_ECUDA.
+ */
+#define MERF_COMM_ID_BYTES 128
+typedef struct merf_comm merf_comm;
+merf_status merf_comm_unique_id(uint8_t *id_out);
+merf_status merf_comm_init(const uint8_t *id, int32_t n_ranks, int32_t rank, int32_t device, merf_comm **out);
+merf_status merf_comm_free(merf_comm *comm);
+merf_status merf_comm_info(const merf_comm *comm, int32_t *n_ranks, int32_t *rank, int32_t *nccl_version);
+merf_status merf_gather_frames(merf_comm *comm, const void *local, void *root_buf, int64_t bytes,
+                               int32_t root, void *stream);
+merf_status merf_comm_wait(merf_comm *comm, void *stream, int32_t timeout_ms);
 
 /*
  * Progressive rendering ("the image is first rendered at a

@@ -11,6 +11,7 @@
 #include <vector>
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: no-ops unless a tool (nsys, ncu --nvtx) attaches
 
 #include "../../include/merf.h"
 #include "merf_device.cuh"
@@ -40,7 +41,22 @@ struct merf_scene {
     merf_kernel_times acc{};
 };
 
+// Every entry point that takes a scene runs on the scene's device: the guard makes it current
+// for the call (kernels, stream-ordered workspaces, grid-size caches) and restores the caller's.
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(const merf_scene* s);
+    ~DeviceGuard() { if (prev >= 0) cudaSetDevice(prev); }
+};
+
 static thread_local std::string g_err;
+
+DeviceGuard::DeviceGuard(const merf_scene* s) {
+    if (!s) return;
+    int cur = 0;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != s->device && cudaSetDevice(s->device) == cudaSuccess)
+        prev = cur;
+}
 
 static merf_status fail(merf_status s, const char* fmt, ...) {
     char buf[512];
@@ -380,6 +396,7 @@ extern "C" merf_status merf_scene_info_get(const merf_scene* s, merf_scene_info*
 extern "C" merf_status merf_scene_occupancy(const merf_scene* s, int32_t level, uint32_t* bits_out,
                                             void* stream) {
     if (!s || !bits_out) return fail(MERF_EINVAL, "NULL argument");
+    DeviceGuard dg(s);
     if (level < 0 || level >= s->desc.n_levels) return fail(MERF_EINVAL, "level out of range");
     CUDA_TRY(cudaMemcpyAsync(bits_out, s->dev.occ[level], occ_words(s->desc.level_res[level]) * 4,
                              cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
@@ -388,6 +405,7 @@ extern "C" merf_status merf_scene_occupancy(const merf_scene* s, int32_t level, 
 
 extern "C" merf_status merf_scene_block_index(const merf_scene* s, int32_t* index_out, void* stream) {
     if (!s || !index_out) return fail(MERF_EINVAL, "NULL argument");
+    DeviceGuard dg(s);
     if (!s->dev.L) return fail(MERF_EINVAL, "scene has no 3D grid");
     int64_t slots = (int64_t)s->dev.nb * s->dev.nb * s->dev.nb;
     CUDA_TRY(cudaMemcpyAsync(index_out, s->dev.block_index, slots * 4, cudaMemcpyDeviceToDevice,
@@ -456,8 +474,17 @@ static merf_status ws_alloc(int64_t n, cudaStream_t st, Workspace& ws, void** ba
     return MERF_OK;
 }
 
+// NVTX range over a host scope (pipeline stage names: "merf_render", "setup", "march", ...),
+// so nsys timelines and `ncu --nvtx --nvtx-include` select the paper's pipeline stages
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+
 static merf_status timed_launch(const merf_scene* cs, uint32_t flags, int kind, cudaStream_t st,
                                 cudaError_t (*fn)(void*), void* arg) {
+    static const char* const kStage[3] = {"merf.setup", "merf.march", "merf.shade"};
+    NvtxRange nv(kStage[kind < 0 || kind > 2 ? 1 : kind]);
     merf_scene* s = const_cast<merf_scene*>(cs);
     if (!(flags & MERF_TIMED)) {
         CUDA_TRY(fn(arg));
@@ -524,6 +551,7 @@ static merf_status run_chunk(const merf_scene* s, int kf_setup, int kf_march, in
 
 extern "C" merf_status merf_kernel_times_get(merf_scene* s, merf_kernel_times* out, int32_t reset) {
     if (!s || !out) return fail(MERF_EINVAL, "NULL argument");
+    DeviceGuard dg(s);
     std::lock_guard<std::mutex> g(s->tmu);
     for (auto& t : s->timed) {
         CUDA_TRY(cudaEventSynchronize(t.b));
@@ -551,6 +579,7 @@ struct Progressive {
 
 struct Shard {
     int rank, count;
+    bool compact;          // output = this part's block slots (merf_render_shard_blocks)
 };
 
 static merf_status render_frames(const merf_scene* s, const merf_camera* cams, int32_t n_cams,
@@ -571,13 +600,15 @@ static merf_status render_frames(const merf_scene* s, const merf_camera* cams, i
         Hl = (H - prog->oy + prog->stride - 1) / prog->stride;
     }
     set_tiles(rs, (Wl + kTileW - 1) / kTileW, ((Wl + kTileW - 1) / kTileW) * ((Hl + kTileH - 1) / kTileH));
-    if (shard && shard->count > 1) {       // 64x64 blocks interleaved by rank
+    if (shard && (shard->count > 1 || shard->compact)) {   // 64x64 blocks interleaved by rank
         rs.part_n = shard->count;
         rs.part_r = shard->rank;
         rs.nbx = (W + 63) / 64;
         rs.n_pblocks = rs.nbx * ((H + 63) / 64);
         const int slots = (rs.n_pblocks + shard->count - 1) / shard->count;
         set_tiles(rs, rs.tiles_x, slots * kShardTiles);
+        rs.compact = shard->compact ? 1 : 0;
+        rs.part_slots = slots;
     }
     const int64_t rays_per_view = (int64_t)rs.tiles_per_view * 32;
     const int cv = chunk_views();
@@ -595,7 +626,8 @@ static merf_status render_frames(const merf_scene* s, const merf_camera* cams, i
         for (int i = 0; i < nv; i++) rs.cb.cam[i] = cams[c0 + i];
         rs.ray0 = 0;
         rs.n = rays_per_view * nv;
-        void* o = (char*)out + (size_t)c0 * W * H * px_bytes;
+        const size_t view_px = rs.compact ? (size_t)rs.part_slots * 4096 : (size_t)W * H;
+        void* o = (char*)out + (size_t)c0 * view_px * px_bytes;
         TraceArgs ta{};
         e = run_chunk(s, count ? KF_COUNT : 0, march_flags(flags, count),
                       format == MERF_RGBA_U8 ? KF_U8 : 0, rs, ws, o, flags, ta, d_stats, st);
@@ -610,6 +642,8 @@ extern "C" merf_status merf_render(const merf_scene* s, const merf_camera* cams,
                                    void* stream, merf_stats* stats) {
     merf_status e = check_frames(s, cams, n_cams, W, H, format, out);
     if (e) return e;
+    DeviceGuard dg(s);
+    NvtxRange nv("merf_render");
     cudaStream_t st = (cudaStream_t)stream;
     unsigned long long* d_stats = nullptr;
     if (stats || (flags & MERF_COUNTERS)) {
@@ -633,10 +667,26 @@ extern "C" merf_status merf_render_shard(const merf_scene* s, const merf_camera*
                                          int32_t format, void* out, uint32_t flags, void* stream) {
     merf_status e = check_frames(s, cams, n_cams, W, H, format, out);
     if (e) return e;
+    DeviceGuard dg(s);
+    NvtxRange nv("merf_render_shard");
     if (part_count < 1 || part_rank < 0 || part_rank >= part_count)
         return fail(MERF_EINVAL, "need 0 <= part_rank < part_count (got %d of %d)", part_rank, part_count);
-    Shard sh{part_rank, part_count};
+    Shard sh{part_rank, part_count, false};
     return render_frames(s, cams, n_cams, W, H, format, out, flags & ~(uint32_t)MERF_COUNTERS,
+                         (cudaStream_t)stream, nullptr, nullptr, &sh);
+}
+
+extern "C" merf_status merf_render_shard_blocks(const merf_scene* s, const merf_camera* cams, int32_t n_cams,
+                                                int32_t W, int32_t H, int32_t part_rank, int32_t part_count,
+                                                int32_t format, void* blocks_out, uint32_t flags, void* stream) {
+    merf_status e = check_frames(s, cams, n_cams, W, H, format, blocks_out);
+    if (e) return e;
+    DeviceGuard dg(s);
+    NvtxRange nv("merf_render_shard_blocks");
+    if (part_count < 1 || part_rank < 0 || part_rank >= part_count)
+        return fail(MERF_EINVAL, "need 0 <= part_rank < part_count (got %d of %d)", part_rank, part_count);
+    Shard sh{part_rank, part_count, true};
+    return render_frames(s, cams, n_cams, W, H, format, blocks_out, flags & ~(uint32_t)MERF_COUNTERS,
                          (cudaStream_t)stream, nullptr, nullptr, &sh);
 }
 
@@ -645,6 +695,8 @@ extern "C" merf_status merf_render_progressive(const merf_scene* s, const merf_c
                                                int32_t format, void* out, uint32_t flags, void* stream) {
     merf_status e = check_frames(s, cams, n_cams, W, H, format, out);
     if (e) return e;
+    DeviceGuard dg(s);
+    NvtxRange nv("merf_render_progressive");
     if (stride < 1 || stride > 64) return fail(MERF_EINVAL, "stride must be in [1, 64]");
     if (pass < 0 || pass >= stride * stride) return fail(MERF_EINVAL, "pass must be in [0, stride^2)");
     Progressive p{stride, pass % stride, pass / stride, fill ? 1 : 0};
@@ -657,6 +709,8 @@ extern "C" merf_status merf_render_host(const merf_scene* cs, const merf_camera*
                                         uint32_t flags, void* stream) {
     merf_status e = check_frames(cs, cams, n_cams, W, H, format, out_host);
     if (e) return e;
+    DeviceGuard dg(cs);
+    NvtxRange nv("merf_render_host");
     merf_scene* s = const_cast<merf_scene*>(cs);
     cudaStream_t st = (cudaStream_t)stream;
     const size_t px_bytes = format == MERF_RGBA_U8 ? 4 : 12;
@@ -726,6 +780,7 @@ extern "C" merf_status merf_render_rays(const merf_scene* s, const double* o, co
                                         const double* t_near, int64_t n, float* rgb, uint32_t flags,
                                         void* stream, merf_stats* stats) {
     if (!s || !o || !d || !rgb) return fail(MERF_EINVAL, "NULL argument");
+    DeviceGuard dg(s);
     if (n < 0 || n > ((int64_t)1 << 31)) return fail(MERF_EINVAL, "bad ray count");
     if (n == 0) return MERF_OK;
     cudaStream_t st = (cudaStream_t)stream;
@@ -770,6 +825,7 @@ extern "C" merf_status merf_trace(const merf_scene* s, const merf_camera* cam, i
                                   uint64_t* cells_out, float* T_out, int32_t* counts_out,
                                   uint32_t flags, void* stream) {
     if (!s || !cam || !pixel_ids || !cells_out || !counts_out) return fail(MERF_EINVAL, "NULL argument");
+    DeviceGuard dg(s);
     if (n < 0 || n > ((int64_t)1 << 31) || W <= 0 || max_per_ray < 0)
         return fail(MERF_EINVAL, "bad n / W / max_per_ray");
     if (!(cam->fx > 0 && cam->fy > 0 && cam->t_near >= 0)) return fail(MERF_EINVAL, "bad camera");
@@ -800,6 +856,7 @@ extern "C" merf_status merf_segments(const merf_scene* s, const merf_camera* cam
                                      const int64_t* pixel_ids, int64_t n, int32_t max_seg,
                                      merf_segment* segs_out, int32_t* counts_out, void* stream) {
     if (!s || !cam || !pixel_ids || !segs_out || !counts_out) return fail(MERF_EINVAL, "NULL argument");
+    DeviceGuard dg(s);
     if (n < 0 || n > ((int64_t)1 << 31) || W <= 0 || max_seg < 0) return fail(MERF_EINVAL, "bad n / W / max_seg");
     if (!(cam->fx > 0 && cam->fy > 0 && cam->t_near >= 0)) return fail(MERF_EINVAL, "bad camera");
     if (n == 0) return MERF_OK;

@@ -6,6 +6,8 @@
 
 namespace merf {
 
+constexpr int kMaxDevices = 64;
+
 static MarchTune march_tune() {
     static MarchTune t = [] {
         MarchTune d{kShadeMin, kTravSteps};
@@ -20,13 +22,18 @@ template <int KF>
 static cudaError_t march_v(const DevScene& S, int64_t n, const Workspace& ws, uint32_t rflags,
                            const TraceArgs& ta, unsigned long long* stats, cudaStream_t st) {
     if (n <= 0) return cudaSuccess;
-    static int blocks = 0;                 // persistent grid: resident CTAs x SMs (per variant)
+    // persistent grid: resident CTAs x SMs, cached per variant and per device (the caller's
+    // entry point has made the scene's device current)
+    static int cache[kMaxDevices] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int blocks = (dev >= 0 && dev < kMaxDevices) ? cache[dev] : 0;
     if (blocks == 0) {
-        int dev = 0, sms = 0, per_sm = 0;
-        cudaGetDevice(&dev);
+        int sms = 0, per_sm = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_kernel<KF>, kMarchThreads, 0);
         blocks = sms * (per_sm > 0 ? per_sm : 1);
+        if (dev >= 0 && dev < kMaxDevices) cache[dev] = blocks;
     }
     int64_t need = (n + kMarchThreads - 1) / kMarchThreads;
     int grid = (int)(need < blocks ? need : blocks);
@@ -49,12 +56,16 @@ static bool use_skiptab(const DevScene& S) {
     return !(e && e[0] && e[0] != '0');
 }
 
+static bool paper_geometry(const DevScene& S) {
+    return S.L == kPaperL && S.R == kPaperR && S.n_fin == kPaperNf && !env_flag("MERF_NO_PAPER");
+}
+
 cudaError_t launch_march(int kf, const DevScene& S, int64_t n, const Workspace& ws, uint32_t rflags,
                          const TraceArgs& ta, unsigned long long* stats, cudaStream_t st) {
     const bool tab = use_skiptab(S);
     if (S.n_src == 4 && !(kf & (KF_TRACE | KF_DENSE))) {    // production variants
         if (tab) {
-            if (S.L == kPaperL && S.R == kPaperR && S.n_fin == kPaperNf && !env_flag("MERF_NO_PAPER")) {
+            if (paper_geometry(S)) {
                 if (kf & KF_COUNT) return march_v<KF_ALLSRC | KF_SKIPTAB | KF_PAPER | KF_COUNT>(S, n, ws, rflags, ta, stats, st);
                 return march_v<KF_ALLSRC | KF_SKIPTAB | KF_PAPER>(S, n, ws, rflags, ta, stats, st);
             }
@@ -63,6 +74,12 @@ cudaError_t launch_march(int kf, const DevScene& S, int64_t n, const Workspace& 
         }
         if (kf & KF_COUNT) return march_v<KF_ALLSRC | KF_COUNT>(S, n, ws, rflags, ta, stats, st);
         return march_v<KF_ALLSRC>(S, n, ws, rflags, ta, stats, st);
+    }
+    // traces: the production instances (the ones merf_render times) plus the trace writes, so
+    // the traversal and gather code of the timed kernel is what the bit-exact trace tests check
+    if (tab && S.n_src == 4 && (kf & (KF_TRACE | KF_DENSE | KF_COUNT)) == KF_TRACE) {
+        if (paper_geometry(S)) return march_v<KF_TRACE | KF_ALLSRC | KF_SKIPTAB | KF_PAPER>(S, n, ws, rflags, ta, stats, st);
+        return march_v<KF_TRACE | KF_ALLSRC | KF_SKIPTAB>(S, n, ws, rflags, ta, stats, st);
     }
     if (tab && (kf & (KF_TRACE | KF_DENSE | KF_COUNT)) == KF_TRACE)
         return march_v<KF_TRACE | KF_SKIPTAB>(S, n, ws, rflags, ta, stats, st);

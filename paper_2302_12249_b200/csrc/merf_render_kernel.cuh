@@ -99,11 +99,14 @@ struct RaySource {
     // exact division by tiles_per_view / tiles_x as a 64-bit multiply-high: m = ceil(2^64 / d)
     // gives floor(n / d) = umulhi(n, m) for all n, d < 2^32 (d >= 2); 0 = not set (divide)
     uint64_t m_tpv, m_tx;
-    // single-frame sharding (merf_render_shard): part_n > 1 -> the rays cover only the
+    // single-frame sharding (merf_render_shard): part_n > 0 -> the rays cover only the
     // 64x64-pixel blocks b with b % part_n == part_r; a view's tile range is then part_slots
     // block slots of kShardTiles tiles (block b = part_r + part_n * slot, row-major over the
     // frame's nbx blocks per row, n_pblocks in total; slots past the last block are empty)
     int part_n, part_r, nbx, n_pblocks;
+    // compact shard output (merf_render_shard_blocks): pixel (px, py) of block b is stored at
+    // [view][slot = b / part_n][py % 64][px % 64] instead of its frame position
+    int compact, part_slots;
 };
 constexpr int kShardBX = 64 / kTileW, kShardBY = 64 / kTileH, kShardTiles = kShardBX * kShardBY;
 
@@ -132,7 +135,7 @@ __device__ __forceinline__ bool ray_pixel(const RaySource& rs, int64_t ray, int&
         tt = (int)(tile - (int64_t)view * rs.tiles_per_view);
     }
     int ty, tx;
-    if (rs.part_n > 1) {
+    if (rs.part_n > 0) {                              // shard modes (set by render_frames)
         const int slot = tt / kShardTiles, w = tt - slot * kShardTiles;
         const int b = rs.part_r + rs.part_n * slot;
         if (b >= rs.n_pblocks) return false;          // padding slot of this shard
@@ -147,6 +150,17 @@ __device__ __forceinline__ bool ray_pixel(const RaySource& rs, int64_t ray, int&
     px = lx * rs.stride_m1 + lx + rs.ox;
     py = ly * rs.stride_m1 + ly + rs.oy;
     return px < rs.W && py < rs.H;
+}
+
+// output element index of a finished pixel: its frame position, or (compact shards) its
+// position in this part's block-slot buffer
+__device__ __forceinline__ int64_t out_index(const RaySource& rs, int view, int px, int py) {
+    if (rs.compact) {
+        const int b = (py >> 6) * rs.nbx + (px >> 6);
+        const int slot = b / rs.part_n;
+        return (((int64_t)view * rs.part_slots + slot) << 12) + ((py & 63) << 6) + (px & 63);
+    }
+    return ((int64_t)view * rs.H + py) * rs.W + px;
 }
 
 struct Workspace {
@@ -869,7 +883,7 @@ __global__ void __launch_bounds__(kSetupThreads) shade_kernel(DevScene S, RaySou
         raygen(rs.cb.cam[view], px, py, od, dd);
 #pragma unroll
         for (int q = 0; q < 3; q++) d[q] = (float)dd[q];
-        out_idx = ((int64_t)view * rs.H + py) * rs.W + px;
+        out_idx = out_index(rs, view, px, py);
     }
     const float4 a0 = ws.accum[r * 2], a1 = ws.accum[r * 2 + 1];
     const float x7[7] = {a0.x, a0.y, a0.z, a1.x, a1.y, a1.z, a1.w};

@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(128) shade_mma_kernel(DevScene S, RaySource rs
         put(ray);
         return;
     }
-    put(((int64_t)view * rs.H + py) * rs.W + px);
+    put(out_index(rs, view, px, py));
     if (rs.fill) {
         // progressive preview: nearest upsampling of the sub-lattice pixel to its
         // stride x stride block (clipped to the frame)

@@ -112,6 +112,16 @@ SIGNATURES = [
     ("merf_scene_load", C.c_int, [C.c_char_p, _i32, C.POINTER(_vp)]),
     ("merf_cameras_read", C.c_int, [C.c_char_p, C.POINTER(merf_camera), _i32, C.POINTER(_i32), _vp, _vp]),
     ("merf_build_block_index", C.c_int, [_vp, C.POINTER(merf_scene_desc), _vp, C.POINTER(_i64), _vp]),
+    ("merf_render_shard_blocks", C.c_int, [_vp, C.POINTER(merf_camera), _i32, _i32, _i32, _i32, _i32, _i32, _vp,
+                                           _u32, _vp]),
+    ("merf_shard_slots", _i32, [_i32, _i32, _i32]),
+    ("merf_shard_assemble", C.c_int, [_vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp]),
+    ("merf_comm_unique_id", C.c_int, [_vp]),
+    ("merf_comm_init", C.c_int, [_vp, _i32, _i32, _i32, C.POINTER(_vp)]),
+    ("merf_comm_free", C.c_int, [_vp]),
+    ("merf_comm_info", C.c_int, [_vp, C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_i32)]),
+    ("merf_gather_frames", C.c_int, [_vp, _vp, _vp, _i64, _i32, _vp]),
+    ("merf_comm_wait", C.c_int, [_vp, _vp, _i32]),
 ]
 
 
@@ -263,6 +273,75 @@ def merf_render_shard(handle, cams, W: int, H: int, part_rank: int, part_count: 
     carr = cameras_to_c(cams)
     _check(lib().merf_render_shard(handle, carr, len(carr), int(W), int(H), int(part_rank), int(part_count),
                                    int(fmt), _ptr(out), int(flags), _stream(stream)))
+
+
+def merf_shard_slots(W: int, H: int, part_count: int) -> int:
+    """64x64 block slots per part of a W x H frame split into part_count parts."""
+    return int(lib().merf_shard_slots(int(W), int(H), int(part_count)))
+
+
+def merf_render_shard_blocks(handle, cams, W: int, H: int, part_rank: int, part_count: int, out,
+                             fmt: int = MERF_RGBA_U8, flags: int = 0, stream=None) -> None:
+    """Render this part's 64x64 blocks into the compact slot buffer `out`
+    ([n_cams][merf_shard_slots][64][64] pixels), ready for merf_gather_frames."""
+    carr = cameras_to_c(cams)
+    _check(lib().merf_render_shard_blocks(handle, carr, len(carr), int(W), int(H), int(part_rank),
+                                          int(part_count), int(fmt), _ptr(out), int(flags), _stream(stream)))
+
+
+def merf_shard_assemble(blocks, n_views: int, W: int, H: int, part_count: int, frame_out,
+                        fmt: int = MERF_RGBA_U8, stream=None) -> None:
+    """Rebuild [n_views][H][W] frames from the gathered [part_count][n_views][slots][64][64] blocks."""
+    _check(lib().merf_shard_assemble(_ptr(blocks), int(n_views), int(W), int(H), int(part_count), int(fmt),
+                                     _ptr(frame_out), _stream(stream)))
+
+
+COMM_ID_BYTES = 128
+
+
+def merf_comm_unique_id() -> bytes:
+    """A new NCCL unique id (rank 0 creates it; the caller distributes it)."""
+    buf = (C.c_uint8 * COMM_ID_BYTES)()
+    _check(lib().merf_comm_unique_id(C.cast(buf, C.c_void_p)))
+    return bytes(buf)
+
+
+class Comm:
+    """The library's NCCL communicator (merf_comm_init / merf_comm_free); the frame gather of
+    SURVEY 8(e) runs through merf_gather_frames on it."""
+
+    def __init__(self, unique_id: bytes, n_ranks: int, rank: int, device: int):
+        assert len(unique_id) == COMM_ID_BYTES
+        buf = (C.c_uint8 * COMM_ID_BYTES).from_buffer_copy(unique_id)
+        h = C.c_void_p()
+        _check(lib().merf_comm_init(C.cast(buf, C.c_void_p), int(n_ranks), int(rank), int(device), C.byref(h)))
+        self.handle = h.value
+        self.n_ranks, self.rank, self.device = n_ranks, rank, device
+
+    def info(self) -> dict:
+        n, r, v = C.c_int32(), C.c_int32(), C.c_int32()
+        _check(lib().merf_comm_info(self.handle, C.byref(n), C.byref(r), C.byref(v)))
+        return {"n_ranks": n.value, "rank": r.value, "nccl_version": v.value}
+
+    def gather(self, local, root_buf, nbytes: int = None, root: int = 0, stream=None) -> None:
+        """merf_gather_frames: `local` (device tensor) of every rank -> root_buf[rank] on the root."""
+        n = int(nbytes if nbytes is not None else local.numel() * local.element_size())
+        _check(lib().merf_gather_frames(self.handle, _ptr(local), _ptr(root_buf), n, int(root), _stream(stream)))
+
+    def wait(self, stream=None, timeout_ms: int = 60000) -> None:
+        """merf_comm_wait: block until `stream` completes, polling NCCL's async error state."""
+        _check(lib().merf_comm_wait(self.handle, _stream(stream), int(timeout_ms)))
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().merf_comm_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def merf_render_host(handle, cams, W: int, H: int, out_host, fmt: int = MERF_RGBA_U8,
@@ -434,7 +513,8 @@ class Scene:
             shape = (n, H, W, 3) if fmt == MERF_RGB_F32 else (n, H, W, 4)
             out = torch.empty(shape, dtype=torch.float32 if fmt == MERF_RGB_F32 else torch.uint8,
                               device=f"cuda:{self.device}")
-        s = merf_render(self.handle, cams, W, H, out, fmt=fmt, flags=flags, stream=stream, stats=stats)
+        with torch.cuda.device(self.device):      # the scene's device's current stream
+            s = merf_render(self.handle, cams, W, H, out, fmt=fmt, flags=flags, stream=stream, stats=stats)
         return (out, s) if stats else out
 
     def close(self):

@@ -143,3 +143,26 @@ def test_product_package_does_not_touch_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 s = open(os.path.join(dp, f)).read()
                 assert "oracle" not in s.lower().replace("no oracle", ""), f
+
+
+def test_comm_unique_id_and_argument_errors(M):
+    """NCCL bootstrap needs no GPU: the unique id is 128 bytes; bad ranks / devices are
+    rejected before any NCCL call (include/merf.h, merf_comm_init)."""
+    uid = M.merf_comm_unique_id()
+    assert isinstance(uid, bytes) and len(uid) == M.merf.COMM_ID_BYTES
+    for n, r in ((1, 1), (2, -1), (0, 0)):
+        with pytest.raises(M.MerfError) as e:
+            M.Comm(uid, n, r, 0)
+        assert e.value.status == M.MERF_EINVAL
+    assert M.merf_shard_slots(1920, 1080, 1) == 30 * 17
+    assert M.merf_shard_slots(1920, 1080, 8) == (30 * 17 + 7) // 8
+    assert M.merf_shard_slots(0, 10, 2) == 0
+
+
+def test_comm_without_nccl_fails_loudly():
+    """No NCCL in the process -> MERF_ENCCL from the comm calls (not a loader error)."""
+    code = ("import paper_2302_12249_b200 as M\n"
+            "try:\n    M.merf_comm_unique_id()\nexcept M.MerfError as e:\n    print('status', e.status)\n")
+    env = dict(os.environ, MERF_NCCL_LIB="/nonexistent/libnccl.so.2")
+    out = subprocess.run(["python", "-c", code], capture_output=True, text=True, env=env, cwd=ROOT, timeout=120)
+    assert "status 4" in out.stdout, out.stdout + out.stderr

@@ -102,3 +102,60 @@ def test_single_frame_shards_combine_world2_gloo():
         assert p.exitcode == 0
     assert (got[..., 3] == 255).all()                        # every pixel from exactly one rank
     assert np.array_equal(got[..., 0], own + 1)
+
+
+def _compact_worker(rank, world, port, q):
+    """each rank packs ITS 64x64 blocks of a synthetic frame into the compact slot layout of
+    merf_render_shard_blocks (include/merf.h), the buffers are gathered to rank 0, and rank 0
+    rebuilds the frame with the layout's index map (what merf_shard_assemble does on the GPU)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import numpy as np
+    W, H, V = 300, 170, 2
+    nbx, nby = (W + 63) // 64, (H + 63) // 64
+    slots = -(-(nbx * nby) // world)
+    rng = np.random.default_rng(5)
+    frame = rng.integers(0, 256, (V, H, W, 4), dtype=np.uint8)       # identical on every rank
+    mine = np.zeros((V, slots, 64, 64, 4), np.uint8)
+    for slot in range(slots):
+        b = rank + world * slot
+        if b >= nbx * nby:
+            continue
+        by, bx = divmod(b, nbx)
+        h, w = min(64, H - by * 64), min(64, W - bx * 64)
+        mine[:, slot, :h, :w] = frame[:, by * 64:by * 64 + h, bx * 64:bx * 64 + w]
+    t = torch.from_numpy(mine)
+    out = [torch.empty_like(t) for _ in range(world)] if rank == 0 else None
+    dist.gather(t, gather_list=out, dst=0)
+    if rank == 0:
+        got = np.zeros_like(frame)
+        seen = np.zeros((H, W), np.int32)
+        for part in range(world):
+            g = out[part].numpy()
+            for slot in range(slots):
+                b = part + world * slot
+                if b >= nbx * nby:
+                    continue
+                by, bx = divmod(b, nbx)
+                h, w = min(64, H - by * 64), min(64, W - bx * 64)
+                got[:, by * 64:by * 64 + h, bx * 64:bx * 64 + w] = g[:, slot, :h, :w]
+                seen[by * 64:by * 64 + h, bx * 64:bx * 64 + w] += 1
+        q.put((bool(np.array_equal(got, frame)), bool((seen == 1).all())))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_compact_shard_gather_assembles_frame_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_compact_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    same, once = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert same and once
