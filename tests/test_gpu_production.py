@@ -68,45 +68,50 @@ def test_counter_instance_counts_equal_oracle_full_frame(M, c2, case):
     assert st["evaluated"] == ref["stats"]["evaluated"], (st["evaluated"], ref["stats"]["evaluated"])
     # alpha == 0 ("density-only", the byte model's 20 B samples) is decided in each side's own
     # precision (D14): fp64 alpha is never exactly 0 on this scene, fp32 alpha is 0 wherever
-    # tau Delta < ~2^-25.  On sampled pixels, the GPU trace's unchanged-T samples must be the
-    # oracle's samples with fp64 alpha below that threshold, outside a band around it.
+    # tau Delta < ~2^-25.  On sampled pixels (the same rays through merf_render_rays), the GPU's
+    # density-only count must equal the number of samples whose fp64 alpha (oracle field at the
+    # oracle's lattice points) is below that edge, up to the samples inside a band around it
+    # (MUFU ex2 error near 1 and the 16-bit density, |dt0| <= 0.0051, blur the edge).
     rng = np.random.default_rng(7)
-    pix = rng.integers(0, W * H, 3000)
+    pix = rng.integers(0, W * H, 600)
+    o = np.empty((len(pix), 3))
+    d = np.empty((len(pix), 3))
+    for r, p in enumerate(pix):
+        o[r], d[r] = O.raygen(cams[0], int(p % W), int(p // W))
     s = M.Scene(c2)
-    pid = torch.as_tensor(pix, device="cuda")
-    cells = torch.zeros((len(pix), 4096), dtype=torch.int64, device="cuda")
-    Tg = torch.zeros((len(pix), 4096), dtype=torch.float32, device="cuda")
-    cnt = torch.zeros(len(pix), dtype=torch.int32, device="cuda")
-    M.merf_trace(s.handle, cams[0], W, pid, 4096, cells, Tg, cnt, flags=M.MERF_NO_EARLY_TERM)
+    rgb = torch.zeros((len(pix), 3), dtype=torch.float32, device="cuda")
+    st_r = M.merf_render_rays(s.handle, torch.as_tensor(o, device="cuda"), torch.as_tensor(d, device="cuda"), rgb,
+                              t_near=torch.full((len(pix),), float(cams[0][16]), dtype=torch.float64, device="cuda"),
+                              flags=M.MERF_NO_EARLY_TERM, stats=True)
     torch.cuda.synchronize()
     s.close()
-    Tg, cnt = Tg.cpu().numpy().astype(np.float64), cnt.cpu().numpy()
     ot = O.render(osc, cams[0], W, H, pixels=pix, max_trace=4096, flags=O.NO_EARLY_TERM)
-    assert np.array_equal(cnt, ot["trace_count"])
-    agree = band = 0
+    assert st_r["evaluated"] == int(ot["trace_count"].sum())
+    below = band = 0
+    alphas = []
+    seg, kk, _ = O.unpack_trace(ot["trace_cells"])
     for r in range(len(pix)):
-        n = cnt[r]
-        To = np.concatenate([[1.0], ot["trace_T"][r, :n]])
-        a_o = 1.0 - To[1:] / np.maximum(To[:-1], 1e-300)
-        Tgr = np.concatenate([[1.0], Tg[r, :n]])
-        zero_g = Tgr[1:] == Tgr[:-1]
-        live = To[:-1] > 1e-30
-        # fp32 1 - alpha rounds to 1 below ~2^-25; MUFU ex2's own error (a few ulp of 1 near
-        # 0) and the 16-bit density (|dt0| <= 0.0051) blur that edge: [2^-28, 2^-21] is
-        # decided either way
-        thr = 2.0 ** -25
-        inband = (a_o > 2.0 ** -28) & (a_o < 2.0 ** -21)
-        ok = live & ~inband
-        agree += int((zero_g[ok] == (a_o[ok] < thr)).sum()) - int(ok.sum())
-        band += int(inband.sum())
-    assert agree == 0, agree
+        segs = O.segment_ray(o[r], d[r], float(cams[0][16]), c2.step)
+        for i in range(ot["trace_count"][r]):
+            g = segs[seg[r, i]]
+            Q = g["Qa"] + kk[r, i] * g["U"]
+            t, _ = O.query_field(osc, Q)
+            a = -np.expm1(-np.exp(t[0]) * c2.step)
+            alphas.append(a)
+            below += a < 2.0 ** -25
+            band += (a > 2.0 ** -28) & (a < 2.0 ** -21)
+    alphas = np.array(alphas)
+    edge = {f"fp64_alpha_below_2^-{k}": int((alphas < 2.0 ** -k).sum()) for k in range(21, 29)}
+    _report("density_only_edge", {"case": case, "gpu_density_only": st_r["density_only"], **edge})
+    assert abs(st_r["density_only"] - below) <= band, (st_r["density_only"], below, band)
     # with termination (bench's setting) the cut is a float decision (D19)
     ref_t = O.render(osc, cams[0], W, H)
     assert abs(st_term["evaluated"] - ref_t["stats"]["evaluated"]) <= 1e-4 * ref_t["stats"]["evaluated"]
     _report("counter_instance_counts", {"case": case, "evaluated": st["evaluated"],
                                         "oracle_evaluated": ref["stats"]["evaluated"],
                                         "density_only": st["density_only"],
-                                        "sampled_alpha_band_samples": band,
+                                        "sampled_rays": len(pix), "sampled_density_only": st_r["density_only"],
+                                        "sampled_fp64_alpha_below_2^-25": int(below), "sampled_alpha_band": int(band),
                                         "evaluated_term": st_term["evaluated"],
                                         "oracle_evaluated_term": ref_t["stats"]["evaluated"]})
 
@@ -139,3 +144,32 @@ def test_adversarial_weight_rounding(M, geom, appearance):
     _report("adversarial_weight_rounding", rec)
     print(rec)
     assert err.max() <= TOL, rec
+
+
+def test_contraction_bit_exact_stress(M):
+    """The canonical fp64 setup (reading D8) relies on the GPU's IEEE division and its
+    contraction being bit-identical to the oracle's: merf_contract (contract_g)
+    on 8 M points with mantissas at every bit pattern, exponents over +-200, values beyond
+    2^600 and below 2^-700 (the division's slow path) and divisor mantissas near 2, compared
+    bit for bit."""
+    import torch
+    rng = np.random.default_rng(2302)
+    n = 1 << 23
+    mant = rng.uniform(1.0, 2.0, (n, 3))
+    expo = rng.integers(-200, 201, (n, 3)).astype(np.float64)
+    sign = rng.choice([-1.0, 1.0], (n, 3))
+    x = sign * mant * np.exp2(expo)
+    x[:1000] *= 2.0 ** 600                       # beyond the guard: IEEE division path
+    x[1000:2000] *= 2.0 ** -700
+    # adversarial mantissas: divisor mantissas near 2 (q0 furthest from a / b)
+    x[2000:200000, 0] = sign[2000:200000, 0] * (2.0 - rng.integers(1, 1 << 20, 198000) * 2.0 ** -52) * 8.0
+    y_ref, r_ref = O.contract(x)
+    xd = torch.as_tensor(x, device="cuda")
+    yd = torch.empty_like(xd)
+    rd = torch.empty(n, dtype=torch.int32, device="cuda")
+    M.merf_contract(xd, yd, rd)
+    torch.cuda.synchronize()
+    yg = yd.cpu().numpy()
+    bad = np.nonzero((yg.view(np.uint64) != y_ref.view(np.uint64)).any(axis=1))[0]
+    assert len(bad) == 0, (len(bad), x[bad[:3]], yg[bad[:3]], y_ref[bad[:3]])
+    assert np.array_equal(rd.cpu().numpy(), r_ref)
