@@ -132,6 +132,24 @@ def _ncu_traffic():
     return _ncu_capture().get("dram_bytes_per_launch")
 
 
+def _capture_current():
+    """does the committed capture describe the library built now?  (source digest stamp)"""
+    try:
+        from paper_2302_12249_b200.build import source_hash
+        cap = _ncu_capture().get("source_sha16")
+        return {"capture_source_sha16": cap, "build_source_sha16": source_hash(),
+                "current": cap is not None and cap == source_hash()}
+    except Exception as e:  # noqa: BLE001
+        return {"current": False, "error": str(e)}
+
+
+def march_instance(info) -> str:
+    """the march template instance merf_render launches for this scene (merf_march.cu)"""
+    paper = info["L"] == 512 and info["R"] == 2048 and list(info["level_res"])[-1] == 256
+    return ("merf::march_kernel<448> (KF_ALLSRC|KF_SKIPTAB|KF_PAPER)" if paper
+            else "merf::march_kernel<192> (KF_ALLSRC|KF_SKIPTAB)")
+
+
 def issue_roofline(avg_launch_ms: float, sm_mhz: float, n_sm: int):
     """The limiter of the march kernel: instruction issue.  achieved = warp instructions per
     launch (ncu, same launch configuration) / (live launch time x SM clock x SMs), against 4
@@ -142,7 +160,7 @@ def issue_roofline(avg_launch_ms: float, sm_mhz: float, n_sm: int):
         return None
     ipc = inst / (avg_launch_ms * 1e-3 * sm_mhz * 1e6 * n_sm)
     return {"bound": "issue", "achieved": ipc, "peak": 4.0, "unit": "warp inst / cycle / SM",
-            "frac": ipc / 4.0, "warp_inst_per_launch": inst,
+            "frac": ipc / 4.0, "warp_inst_per_launch": inst, "capture": _capture_current(),
             "source": "instruction count: " + cap.get("source", "profiles/render_traffic.json")
                       + "; time: live CUDA events of this run; clock: nvidia-smi median during the run"}
 
@@ -327,6 +345,12 @@ def main():
             n_seg += st["segments"]
             region_segs = [a + b for a, b in zip(region_segs, st["region_segments"])]
     rays_per_step = V * W_IMG * H_IMG
+    ws = M.merf_render_workspace_bytes(scene.handle, V, W_IMG, H_IMG)
+    vram = {"scene_device_bytes": info["device_bytes"], "baked_arrays_bytes": int(sc.nbytes()),
+            "render_workspace_bytes": ws["bytes"], "workspace_bytes_per_ray": ws["bytes_per_ray"],
+            "frame_buffers_bytes": 2 * V * H_IMG * W_IMG * 4,
+            "note": "scene = every device layout built at upload (DESIGN 5); workspace = one merf_render "
+                    "chunk (7 segment slots + accumulators per ray)"}
 
     gathered = [torch.cuda.Event() for _ in range(2)]   # buffer b's last gather finished
 
@@ -401,9 +425,16 @@ def main():
     avg_launch_ms = kt["march_ms"] / n_march
     bytes_per_launch = sum(algo_bytes) / n_march
     achieved = bytes_per_launch / (avg_launch_ms / 1e3) / 1e9
+    traffic = _ncu_traffic()
+    dram_gbs = traffic / (avg_launch_ms / 1e3) / 1e9 if traffic else None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": _ncu_traffic(), "peak_source": peak_src,
-                "kernel": "merf::march_kernel<KF_ALLSRC> (persistent march: traversal + gather + composite)",
+                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                "achieved_is": "algorithmic gather rate: the texel bytes the method reads (SURVEY 8(d) "
+                               "model) / live launch time; served mostly by L1/L2, not HBM",
+                "dram_gbs": dram_gbs, "dram_frac": dram_gbs / peak if dram_gbs else None,
+                "dram_source": "ncu dram bytes per launch (profiles/render_traffic.json) / live launch time",
+                "capture": _capture_current(),
+                "kernel": march_instance(info) + " (persistent march: traversal + gather + composite)",
                 "avg_launch_ms": avg_launch_ms, "launches": kt["march_launches"],
                 "algorithmic_bytes_per_launch": bytes_per_launch,
                 "bytes_model": "160 B per evaluated sample with alpha > 0, 20 B per density-only "
@@ -461,13 +492,16 @@ def main():
                                    + ("_spherical_contraction" if args.spherical else ""),
                        "views_per_rank_per_step": V, "W": W_IMG, "H": H_IMG,
                        "scene": {k: info[k] for k in ("L", "R", "level_res", "n_blocks", "device_bytes")},
+                       "vram": vram,
                        "block_fraction": info["n_blocks"] / (info["L"] // 8) ** 3 if info["L"] else None,
                        "finest_occupancy_fraction": occ_frac,
                        "l2": "no flush: inputs (scene %.0f MB) larger than the 126 MB L2; each step renders "
                              "different orbit views" % (info["device_bytes"] / 1e6),
                        "parallelism": f"views sharded over {world} rank(s), scene replicated, "
                                       "NCCL frame gather to rank 0",
-                       "dtype_detail": "u8 features, fp64 ray setup, int32 lattice, fp32 shading (appearance: 16-bit fixed-point weights + dp2a)"},
+                       "dtype_detail": "u8 features; fp64 ray setup; int32 lattice; interpolation with 16-bit "
+                                       "fixed-point weights (dp2a integer sums, exact partition); fp32 decode, "
+                                       "composite and MLP accumulation; MLP operands split-fp16 mma.sync"},
             "fps": value / (W_IMG * H_IMG),
             "fps_per_gpu": value / (W_IMG * H_IMG) / world,
             "samples_per_sec": n_eval * world / (ms / 1e3),

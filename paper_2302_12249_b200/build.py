@@ -28,6 +28,19 @@ def _deps():
             + [os.path.join(ROOT, "include", "merf.h"), __file__])
 
 
+def source_hash() -> str:
+    """16-hex digest of the library sources (csrc + include/merf.h): stamps profile captures so
+    that bench.py can tell whether a committed ncu capture still describes the built kernels."""
+    import hashlib
+    h = hashlib.sha256()
+    for p in sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cuh"))
+                    + glob.glob(os.path.join(CSRC, "*.h")) + [os.path.join(ROOT, "include", "merf.h")]):
+        h.update(os.path.basename(p).encode())
+        with open(p, "rb") as f:
+            h.update(f.read())
+    return h.hexdigest()[:16]
+
+
 def needs_build() -> bool:
     if not os.path.exists(LIB):
         return True

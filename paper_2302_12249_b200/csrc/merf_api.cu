@@ -459,13 +459,19 @@ static int chunk_views() {
 
 static size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 
+// workspace bytes of a chunk of n rays (shared with
+// merf_render_workspace_bytes so that the reported figure is the allocated one)
+static size_t ws_bytes(int64_t n) {
+    return align256((size_t)n * kMaxSeg * 32) + align256((size_t)n) + align256((size_t)n * 32) + 256;
+}
+
 static merf_status ws_alloc(int64_t n, cudaStream_t st, Workspace& ws, void** base) {
     const size_t seg = align256((size_t)n * kMaxSeg * 32);
     const size_t ns = align256((size_t)n);
     const size_t acc = align256((size_t)n * 32);
-    CUDA_TRY(cudaMallocAsync(base, seg + ns + acc + 256, st));
+    CUDA_TRY(cudaMallocAsync(base, ws_bytes(n), st));
     static const bool poison = getenv("MERF_DEBUG_POISON") != nullptr;   // debug: NaN-fill
-    if (poison) CUDA_TRY(cudaMemsetAsync(*base, 0xFF, seg + ns + acc + 256, st));
+    if (poison) CUDA_TRY(cudaMemsetAsync(*base, 0xFF, ws_bytes(n), st));
     char* b = (char*)*base;
     ws.seg = (int4*)b;
     ws.nseg = (uint8_t*)(b + seg);
@@ -659,6 +665,20 @@ extern "C" merf_status merf_render(const merf_scene* s, const merf_camera* cams,
         CUDA_TRY(cudaStreamSynchronize(st));
         if (stats) to_stats(h, stats);
     }
+    return MERF_OK;
+}
+
+extern "C" merf_status merf_render_workspace_bytes(const merf_scene* s, int32_t n_cams, int32_t W, int32_t H,
+                                                   int64_t* bytes, int64_t* rays_per_chunk) {
+    if (!s || !bytes || n_cams <= 0 || W <= 0 || H <= 0) return fail(MERF_EINVAL, "bad arguments");
+    const int64_t tiles = (int64_t)((W + kTileW - 1) / kTileW) * ((H + kTileH - 1) / kTileH);
+    const int64_t rays_per_view = tiles * 32;
+    const int cv = chunk_views();
+    int64_t vpc = kChunkRays * cv / kViewsPerChunk / rays_per_view;
+    vpc = vpc < 1 ? 1 : (vpc > cv ? cv : vpc);
+    if (vpc > n_cams) vpc = n_cams;
+    *bytes = (int64_t)ws_bytes(rays_per_view * vpc);
+    if (rays_per_chunk) *rays_per_chunk = rays_per_view * vpc;
     return MERF_OK;
 }
 

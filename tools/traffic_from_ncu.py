@@ -7,7 +7,17 @@ import argparse
 import csv
 import io
 import json
+import os
 import subprocess
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def _source_hash():
+    """the library-source digest the capture was taken with (paper_2302_12249_b200.build)"""
+    from paper_2302_12249_b200.build import source_hash
+    return source_hash()
 
 
 def main():
@@ -32,7 +42,8 @@ def main():
          "warp_inst_per_launch": float(r["smsp__inst_executed.sum"]),
          "l2_bytes_per_launch": 32.0 * float(r["lts__t_sectors.sum"]),
          "sm_cycles_per_launch": float(r["sm__cycles_elapsed.avg"]),
-         "note": "includes the workspace (segments read, accumulators written); scene texels hit L1/L2"}
+         "note": "includes the workspace (segments read, accumulators written); scene texels hit L1/L2",
+         "source_sha16": _source_hash()}
     with open(a.out, "w") as f:
         json.dump(d, f, indent=1)
     print(json.dumps(d))
