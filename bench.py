@@ -215,7 +215,8 @@ def run_reference(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "orbit1080p_paper_scale_merf" + ("_dense_ablation" if args.dense else "")
                         + ("_mlp_ffma_ablation" if getattr(args, "mlp_ffma", False) else "")
-                                   + ("_spherical_contraction" if args.spherical else ""), "scene": "c2 (512^3 sparse grid, 3x2048^2 planes)",
+                                   + ("_spherical_contraction" if args.spherical else "")
+                                   + ("_persistent_fp32" if getattr(args, "sph_persistent", False) else ""), "scene": "c2 (512^3 sparse grid, 3x2048^2 planes)",
                        "sample": f"every {stride}th pixel of one 1920x1080 orbit view per step"},
             "cpu_baseline": {"value": value, "unit": "rays/s", "cores": O.max_threads(), "kind": "oracle",
                              "sample": f"every {stride}th pixel of one 1920x1080 orbit view per step"},
@@ -288,6 +289,9 @@ def main():
     ap.add_argument("--spherical", action="store_true",
                     help="NEXT-2 comparison: the scene baked in the spherical contraction's space, "
                          "rendered with fixed contracted-arc-length steps and no AABB skipping")
+    ap.add_argument("--sph-persistent", action="store_true",
+                    help="with --spherical: the curve march in fp32 inside the persistent tile-scheduled "
+                         "march kernel (like-for-like with the contract_pi path)")
     ap.add_argument("--dense", action="store_true",
                     help="ablation: dense lattice stepping gated by the finest level (no skipping)")
     ap.add_argument("--mlp-ffma", action="store_true",
@@ -321,6 +325,7 @@ def main():
     batches = [orbit_cameras(N_ORBIT, indices=views_for(rank, world, s, V)) for s in range(steps_total)]
 
     extra_flags = ((M.MERF_DENSE if args.dense else 0) | (M.MERF_SPHERICAL if args.spherical else 0)
+                   | (M.MERF_SPH_PERSISTENT if args.sph_persistent else 0)
                    | (M.MERF_MLP_FFMA if args.mlp_ffma else 0))
     stream = torch.cuda.Stream()
     gstream = torch.cuda.Stream()
@@ -489,7 +494,8 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": "orbit1080p_paper_scale_merf" + ("_dense_ablation" if args.dense else "")
                         + ("_mlp_ffma_ablation" if getattr(args, "mlp_ffma", False) else "")
-                                   + ("_spherical_contraction" if args.spherical else ""),
+                                   + ("_spherical_contraction" if args.spherical else "")
+                                   + ("_persistent_fp32" if getattr(args, "sph_persistent", False) else ""),
                        "views_per_rank_per_step": V, "W": W_IMG, "H": H_IMG,
                        "scene": {k: info[k] for k in ("L", "R", "level_res", "n_blocks", "device_bytes")},
                        "vram": vram,

@@ -74,10 +74,16 @@ enum {
                                   every sample tested against the finest level, no AABB skip
                                   (P:222-226).  Accepted by merf_render, merf_render_rays,
                                   merf_trace (segment ordinal 0, k = step index).            */
-    MERF_MLP_FFMA = 32u        /* run the deferred MLP (Eq. 3) as FFMA chains instead of
+    MERF_MLP_FFMA = 32u,       /* run the deferred MLP (Eq. 3) as FFMA chains instead of
                                   the default tensor-core kernel (split-fp16 mma.sync, fp32-class
                                   accuracy); cross-check / ablation.  Scenes whose MLP weights
                                   could overflow fp16 always use the FFMA kernel.              */
+    MERF_SPH_PERSISTENT = 64u  /* with MERF_SPHERICAL in merf_render / merf_render_rays: the
+                                  same curve march in fp32 inside the persistent tile-scheduled
+                                  march kernel with the production gather -- the like-for-like
+                                  speed comparison with the piecewise-projective contraction.
+                                  fp32 sample positions differ slightly from the canonical fp64
+                                  steps, so its parity is statistical (traces: fp64 kernel).  */
 };
 
 #define MERF_MAX_LEVELS 4
@@ -115,6 +121,8 @@ typedef struct {
     int64_t march_rounds;       /* warp shading rounds of the persistent march (perf counter) */
     int64_t march_steps;        /* warp traversal iterations (perf counter)                   */
     int64_t march_lane_rounds;  /* sum over rounds of lanes holding a ray (perf counter)      */
+    int64_t march_busy_ns;      /* per march launch, summed: first warp start -> tile queue dry */
+    int64_t march_tail_ns;      /* per march launch, summed: tile queue dry -> last warp exit   */
 } merf_stats;
 
 typedef struct {

@@ -437,6 +437,8 @@ static void to_stats(const unsigned long long* h, merf_stats* st) {
     st->march_rounds = (int64_t)h[13];
     st->march_steps = (int64_t)h[14];
     st->march_lane_rounds = (int64_t)h[15];
+    st->march_busy_ns = (int64_t)h[19];
+    st->march_tail_ns = (int64_t)h[20];
 }
 
 // ------------------------------------------------------------------------------------
@@ -461,8 +463,33 @@ static size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 
 // workspace bytes of a chunk of n rays (shared with
 // merf_render_workspace_bytes so that the reported figure is the allocated one)
+static size_t ws_tiles(int64_t n) { return (size_t)((n + 31) / 32); }
 static size_t ws_bytes(int64_t n) {
-    return align256((size_t)n * kMaxSeg * 32) + align256((size_t)n) + align256((size_t)n * 32) + 256;
+    return align256((size_t)n * kMaxSeg * 32) + align256((size_t)n) + align256((size_t)n * 32) + 256
+           + align256(ws_tiles(n) * kBuckets * 4) + 256;
+}
+
+// Tile dispatch order.  Cost-ordered (longest first, Workspace::tile_list) for launches of at
+// most kLptMaxViews views, raster order otherwise.  Measured on 1080p orbit views (bench
+// workload, tools/view_scaling.py): the march's tail (tile queue dry -> last warp exit) drops
+// from 0.36-0.47 ms to 0.10-0.17 ms for 2-16 views and the march per view by 1-6 %, but the
+// estimate costs 0.035-0.04 ms of setup per view, so it pays only while the tail is a large
+// share of the launch (1-4 views: 1.8 % to 6 % faster per view); at 16 views it is a 2 % loss.
+// MERF_TILE_ORDER=raster / cost forces either order (A/B).
+static const int kLptMaxViews = 4;
+static int tile_order_override() {                   // 0 = policy, 1 = raster, 2 = cost
+    static const int v = [] {
+        const char* e = getenv("MERF_TILE_ORDER");
+        if (!e) return 0;
+        if (!strcmp(e, "raster")) return 1;
+        if (!strcmp(e, "cost")) return 2;
+        return 0;
+    }();
+    return v;
+}
+static bool cost_order(int views_per_chunk) {
+    const int o = tile_order_override();
+    return o == 2 || (o == 0 && views_per_chunk <= kLptMaxViews);
 }
 
 static merf_status ws_alloc(int64_t n, cudaStream_t st, Workspace& ws, void** base) {
@@ -477,6 +504,9 @@ static merf_status ws_alloc(int64_t n, cudaStream_t st, Workspace& ws, void** ba
     ws.nseg = (uint8_t*)(b + seg);
     ws.accum = (float4*)(b + seg + ns);
     ws.queue = (unsigned int*)(b + seg + ns + acc);
+    ws.bucket_cnt = (unsigned int*)(b + seg + ns + acc + 128);
+    ws.tile_list = (int*)(b + seg + ns + acc + 256);   // cost order available; the caller may clear it
+    ws.n_tiles = (int)ws_tiles(n);
     return MERF_OK;
 }
 
@@ -539,8 +569,15 @@ static cudaError_t call_shade(void* p) {
 }
 
 static merf_status run_chunk(const merf_scene* s, int kf_setup, int kf_march, int kf_shade,
-                             const RaySource& rs, const Workspace& ws, void* out, uint32_t flags,
+                             const RaySource& rs, const Workspace& ws_in, void* out, uint32_t flags,
                              const TraceArgs& ta, unsigned long long* d_stats, cudaStream_t st) {
+    Workspace ws = ws_in;
+    ws.n_tiles = (int)ws_tiles(rs.n);                 // this chunk's tiles
+    if ((flags & MERF_SPHERICAL) && (flags & MERF_SPH_PERSISTENT) && !(kf_setup & (KF_TRACE | KF_SEGS))) {
+        kf_setup |= KF_SPH;                // like-for-like: the persistent pipeline, fp32 curve steps
+        if (kf_march >= 0) kf_march = KF_SPH | (kf_march & KF_COUNT);
+        flags &= ~(uint32_t)MERF_SPHERICAL;
+    }
     ChunkCall c{s, kf_setup, kf_march, kf_shade, &rs, &ws, out, flags, &ta, d_stats, st};
     if (flags & MERF_SPHERICAL) {          // NEXT-2 variant: no setup kernel, one march kernel
         merf_status e = timed_launch(s, flags, 1, st, call_march_sph, &c);
@@ -548,9 +585,11 @@ static merf_status run_chunk(const merf_scene* s, int kf_setup, int kf_march, in
         if (kf_shade >= 0 && (e = timed_launch(s, flags, 2, st, call_shade, &c))) return e;
         return MERF_OK;
     }
+    if (ws.tile_list) CUDA_TRY(cudaMemsetAsync(ws.bucket_cnt, 0, kBuckets * sizeof(unsigned int), st));
     merf_status e = timed_launch(s, flags, 0, st, call_setup, &c);
     if (e) return e;
     if (kf_march >= 0 && (e = timed_launch(s, flags, 1, st, call_march, &c))) return e;
+    if (kf_march >= 0 && d_stats) CUDA_TRY(launch_stats_fold(d_stats, st));
     if (kf_shade >= 0 && (e = timed_launch(s, flags, 2, st, call_shade, &c))) return e;
     return MERF_OK;
 }
@@ -625,6 +664,7 @@ static merf_status render_frames(const merf_scene* s, const merf_camera* cams, i
     void* base = nullptr;
     merf_status e = ws_alloc(rays_per_view * vpc, st, ws, &base);
     if (e) return e;
+    if (!cost_order(vpc)) ws.tile_list = nullptr;
     const bool count = d_stats != nullptr;
     for (int c0 = 0; c0 < n_cams; c0 += vpc) {
         const int nv = n_cams - c0 < vpc ? n_cams - c0 : vpc;
@@ -653,13 +693,14 @@ extern "C" merf_status merf_render(const merf_scene* s, const merf_camera* cams,
     cudaStream_t st = (cudaStream_t)stream;
     unsigned long long* d_stats = nullptr;
     if (stats || (flags & MERF_COUNTERS)) {
-        CUDA_TRY(cudaMallocAsync(&d_stats, 16 * sizeof(unsigned long long), st));
-        CUDA_TRY(cudaMemsetAsync(d_stats, 0, 16 * sizeof(unsigned long long), st));
+        CUDA_TRY(cudaMallocAsync(&d_stats, kStatWords * sizeof(unsigned long long), st));
+        CUDA_TRY(cudaMemsetAsync(d_stats, 0, kStatWords * sizeof(unsigned long long), st));
+        CUDA_TRY(cudaMemsetAsync(d_stats + 16, 0xFF, 2 * sizeof(unsigned long long), st));   // min slots
     }
     e = render_frames(s, cams, n_cams, W, H, format, out, flags, st, d_stats);
     if (e) return e;
     if (d_stats) {
-        unsigned long long h[16];
+        unsigned long long h[kStatWords];
         CUDA_TRY(cudaMemcpyAsync(h, d_stats, sizeof(h), cudaMemcpyDeviceToHost, st));
         CUDA_TRY(cudaFreeAsync(d_stats, st));
         CUDA_TRY(cudaStreamSynchronize(st));
@@ -806,8 +847,9 @@ extern "C" merf_status merf_render_rays(const merf_scene* s, const double* o, co
     cudaStream_t st = (cudaStream_t)stream;
     unsigned long long* d_stats = nullptr;
     if (stats) {
-        CUDA_TRY(cudaMallocAsync(&d_stats, 16 * sizeof(unsigned long long), st));
-        CUDA_TRY(cudaMemsetAsync(d_stats, 0, 16 * sizeof(unsigned long long), st));
+        CUDA_TRY(cudaMallocAsync(&d_stats, kStatWords * sizeof(unsigned long long), st));
+        CUDA_TRY(cudaMemsetAsync(d_stats, 0, kStatWords * sizeof(unsigned long long), st));
+        CUDA_TRY(cudaMemsetAsync(d_stats + 16, 0xFF, 2 * sizeof(unsigned long long), st));   // min slots
     }
     {
         RaySource rs{};
@@ -819,6 +861,7 @@ extern "C" merf_status merf_render_rays(const merf_scene* s, const double* o, co
         void* base = nullptr;
         merf_status e = ws_alloc(chunk, st, ws, &base);
         if (e) return e;
+        if (tile_order_override() != 2) ws.tile_list = nullptr;   // explicit rays: caller's order
         const bool count = d_stats != nullptr;
         for (int64_t c0 = 0; c0 < n; c0 += chunk) {
             rs.ray0 = c0;
@@ -831,7 +874,7 @@ extern "C" merf_status merf_render_rays(const merf_scene* s, const double* o, co
         CUDA_TRY(cudaFreeAsync(base, st));
     }
     if (d_stats) {
-        unsigned long long h[16];
+        unsigned long long h[kStatWords];
         CUDA_TRY(cudaMemcpyAsync(h, d_stats, sizeof(h), cudaMemcpyDeviceToHost, st));
         CUDA_TRY(cudaFreeAsync(d_stats, st));
         CUDA_TRY(cudaStreamSynchronize(st));
@@ -863,6 +906,7 @@ extern "C" merf_status merf_trace(const merf_scene* s, const merf_camera* cam, i
         void* base = nullptr;
         merf_status e = ws_alloc(n, st, ws, &base);
         if (e) return e;
+        ws.tile_list = nullptr;                      // pixel lists: the caller's order
         TraceArgs ta{cells_out, T_out, counts_out, max_per_ray, nullptr};
         e = run_chunk(s, KF_TRACE, KF_TRACE | ((flags & MERF_DENSE) ? KF_DENSE : 0), -1, rs, ws, nullptr,
                       flags, ta, nullptr, st);
@@ -1034,6 +1078,7 @@ extern "C" merf_status merf_qat_step(const merf_qat_desc* d, const float* theta_
     if (ce == cudaSuccess) ce = cudaMemsetAsync(loss, 0, 8, st);
     if (ce == cudaSuccess && n_samples) ce = cudaMemsetAsync(n_samples, 0, 8, st);
     TraceArgs ta{};
+    ws.tile_list = nullptr;                          // the QAT kernels walk rays in raster order
     if (ce == cudaSuccess) ce = launch_setup(0, S, rs, ws, ta, nullptr, st);
     if (ce == cudaSuccess)
         ce = launch_qat(S, rs, ws, theta_v, theta_p, vv, vp, d->quantize ? 1 : 0, target, rgb_out, gvv, gvp,

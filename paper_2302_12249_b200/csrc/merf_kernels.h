@@ -61,5 +61,6 @@ cudaError_t launch_qat(const DevScene& S, const RaySource& rs, const Workspace& 
                        float* rayb, const float* mlp, double* loss, unsigned int* overflow,
                        unsigned long long* n_samples, int L, int R, int Nf, const uint32_t* occf, float md, float ma,
                        cudaStream_t st);
+cudaError_t launch_stats_fold(unsigned long long* stats, cudaStream_t st);
 
 }  // namespace merf

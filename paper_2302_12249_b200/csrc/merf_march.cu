@@ -43,6 +43,22 @@ static cudaError_t march_v(const DevScene& S, int64_t n, const Workspace& ws, ui
     return cudaGetLastError();
 }
 
+// fold one launch's (start, dry, end) timestamps into the busy / tail sums and re-arm them
+__global__ void stats_fold_kernel(unsigned long long* st) {
+    if (st[16] != ~0ull && st[17] != ~0ull && st[18] >= st[17] && st[17] >= st[16]) {
+        st[19] += st[17] - st[16];
+        st[20] += st[18] - st[17];
+    }
+    st[16] = ~0ull;
+    st[17] = ~0ull;
+    st[18] = 0;
+}
+
+cudaError_t launch_stats_fold(unsigned long long* stats, cudaStream_t st) {
+    stats_fold_kernel<<<1, 1, 0, st>>>(stats);
+    return cudaGetLastError();
+}
+
 static bool env_flag(const char* name) {
     const char* e = getenv(name);
     return e && e[0] && e[0] != '0';
@@ -62,6 +78,14 @@ static bool paper_geometry(const DevScene& S) {
 
 cudaError_t launch_march(int kf, const DevScene& S, int64_t n, const Workspace& ws, uint32_t rflags,
                          const TraceArgs& ta, unsigned long long* stats, cudaStream_t st) {
+    if (kf & KF_SPH) {                                // NEXT-2 like-for-like variant
+        if (S.n_src == 4 && paper_geometry(S)) {
+            if (kf & KF_COUNT) return march_v<KF_SPH | KF_ALLSRC | KF_PAPER | KF_COUNT>(S, n, ws, rflags, ta, stats, st);
+            return march_v<KF_SPH | KF_ALLSRC | KF_PAPER>(S, n, ws, rflags, ta, stats, st);
+        }
+        if (kf & KF_COUNT) return march_v<KF_SPH | KF_COUNT>(S, n, ws, rflags, ta, stats, st);
+        return march_v<KF_SPH>(S, n, ws, rflags, ta, stats, st);
+    }
     const bool tab = use_skiptab(S);
     if (S.n_src == 4 && !(kf & (KF_TRACE | KF_DENSE))) {    // production variants
         if (tab) {

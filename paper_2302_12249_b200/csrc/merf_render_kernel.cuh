@@ -36,6 +36,8 @@ enum : int {
     KF_ALLSRC = 64,     // all four sources present (compile-time; the production variant)
     KF_SKIPTAB = 128,   // skip level from the per-cell table (S.skiptab) instead of the level search
     KF_PAPER = 256,     // the paper's default resolutions as compile-time constants (below)
+    KF_SPH = 512,       // NEXT-2 like-for-like: spherical contraction, fp32 curve stepping in the
+                        // persistent tile-scheduled march (MERF_SPHERICAL | MERF_SPH_PERSISTENT)
 };
 
 // The paper's default scene geometry (L = 512, R = 2048; finest occupancy level
@@ -163,12 +165,38 @@ __device__ __forceinline__ int64_t out_index(const RaySource& rs, int view, int 
     return ((int64_t)view * rs.H + py) * rs.W + px;
 }
 
+// Tile dispatch order of the persistent march (longest-processing-time first).  The march's
+// tail -- from the moment its tile queue runs dry to the last warp's exit -- is the duration
+// of the most expensive tiles taken last (measured 0.36-0.47 ms per launch on the orbit views,
+// 23 % of a single 1080p view: 1 % of the tiles have a ray with >= 268 evaluated samples, 5x the
+// median tile, and take ~1 ms under full load).  The setup kernel therefore estimates every
+// 32-ray tile's cost (tile_cost_bucket) and appends the tile to one of kBuckets lists by log2 of
+// the estimate; the march takes the lists most expensive first.  The order changes no ray's
+// arithmetic: every tile is still marched by one warp.
+constexpr int kBuckets = 8;
+
 struct Workspace {
     int4* seg;                   // [n][kMaxSeg][2]: (Qa.xyz, K), (U.xyz, region)
     uint8_t* nseg;               // [n]
     float4* accum;               // [n][2]: (C_d.rgb, T), (F0..F3)
-    unsigned int* queue;         // ray counter of the persistent march
+    unsigned int* queue;         // tile counter of the persistent march
+    int* tile_list;              // [kBuckets][n_tiles] tile indices, or NULL: raster order
+    unsigned int* bucket_cnt;    // [kBuckets] tiles per list (zeroed before the setup)
+    int n_tiles;                 // ceil(n / 32) of the current chunk
 };
+
+
+
+// merf_stats counters (device array of kStatWords): 0..15 as merf_stats; per march launch
+// 16 = first warp start, 17 = first warp to find the tile queue empty, 18 = last warp exit
+// (%globaltimer ns, min/min/max), folded into 19 (busy) and 20 (tail) sums after each launch
+constexpr int kStatWords = 24;
+
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 struct TraceArgs {
     uint64_t* cells;
@@ -186,6 +214,86 @@ __device__ __forceinline__ void add_stat(unsigned long long* stats, int idx, int
 // ====================================================================================
 // 1. setup
 // ====================================================================================
+// Tile-cost estimate for the dispatch order (not part of the rendered result): the tile's
+// centre ray (lane kCostLane) is probed at 64 points spread evenly over its lattice samples, two
+// per lane.  An occupied probe stands for Ktot/64 samples; its optical depth is estimated from
+// the NEAREST texel of each source (no interpolation weights) and the probes are counted in ray
+// order until the accumulated optical depth passes ln(1/t_min), where termination would cut the
+// ray.  Measured on a 1080p orbit view (tools/tile_cost.py): rank correlation 0.54 with the
+// tile's true longest ray, and all of the 1 % most expensive tiles land in the top two buckets
+// (a two-probes-per-segment occupancy count without the density term: -0.25, and 73 % of them
+// in the cheapest bucket).
+constexpr int kCostLane = 20;      // pixel (4, 2) of the 8x4 tile
+
+__device__ __forceinline__ float probe_od(const DevScene& S, int Qx, int Qy, int Qz, float od_per_tau) {
+    const int N = S.n_fin, sf = S.s_fin;
+    if (!occ_bit(S.occ_fin, occ_cell(Qx, sf, N), occ_cell(Qy, sf, N), occ_cell(Qz, sf, N), N)) return -1.f;
+    unsigned sum = 0;
+    int n = 0;
+    if (S.use_v) {
+        const int L = S.L;
+        const int ix = min(max(Qx >> S.sV, 0), L - 1), iy = min(max(Qy >> S.sV, 0), L - 1),
+                  iz = min(max(Qz >> S.sV, 0), L - 1);
+        const int blk = __ldg(S.block_index + ((iz >> 3) * S.nb + (iy >> 3)) * S.nb + (ix >> 3));
+        if (blk >= 0) {
+            sum += __ldg(S.vdens + (unsigned)(blk * 512 + ((iz & 7) * 8 + (iy & 7)) * 8 + (ix & 7))).x & 0xFFu;
+            n++;
+        }
+    }
+    if (S.R > 0) {
+        const int R = S.R;
+        const int px = min(max(Qx >> S.sP, 0), R - 1), py = min(max(Qy >> S.sP, 0), R - 1),
+                  pz = min(max(Qz >> S.sP, 0), R - 1);
+        const int v[3] = {pz, pz, py}, u[3] = {py, px, px};
+#pragma unroll
+        for (int a = 0; a < 3; a++)
+            if (S.use_p[a]) {
+                sum += __ldg(S.pdens + ((unsigned)(a * R + v[a]) * R + u[a])) & 0xFFu;
+                n++;
+            }
+    }
+    // tau Delta = 2^(s kd_l2 - n md_l2 + log2 Delta), times the samples the probe stands for
+    return ex2_ftz(fmaf((float)sum, S.kd_l2, fmaf((float)n, -S.md_l2, S.log2_step))) * od_per_tau;
+}
+
+// bucket of the tile that holds chunk-local ray r (call with all 32 lanes of the warp, after the
+// warp's segments are in the workspace)
+__device__ __forceinline__ int tile_cost_bucket(const DevScene& S, const Workspace& ws, int64_t r, int64_t n) {
+    const int lane = threadIdx.x & 31;
+    const int64_t rc = (r & ~(int64_t)31) + kCostLane;
+    int ns = 0;
+    if (rc < n) ns = ws.nseg[rc];
+    const int4* sp = ws.seg + rc * kMaxSeg * 2;
+    int Ktot = 0;
+    for (int j = 0; j < ns; j++) Ktot += sp[2 * j].w;            // uniform loop (same ray)
+    float od[2] = {-1.f, -1.f};
+    const float per = (float)Ktot * (1.f / 64.f);
+    if (Ktot > 0) {
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            int k = (int)(((float)(2 * lane + h) + 0.5f) * per);
+            int j = 0;
+            while (j < ns - 1 && k >= sp[2 * j].w) { k -= sp[2 * j].w; j++; }
+            const int4 qa = sp[2 * j], uu = sp[2 * j + 1];
+            od[h] = probe_od(S, qa.x + k * uu.x, qa.y + k * uu.y, qa.z + k * uu.z, per);
+        }
+    }
+    // optical depth accumulated before each probe, in ray order (lane-major): exclusive scan
+    const float mine = fmaxf(od[0], 0.f) + fmaxf(od[1], 0.f);
+    float inc = mine;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const float v = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += v;
+    }
+    const float before0 = inc - mine, before1 = before0 + fmaxf(od[0], 0.f);
+    const float cut = -__logf(S.t_min);
+    const int cnt = (od[0] >= 0.f && before0 < cut) + (od[1] >= 0.f && before1 < cut);
+    const int tot = __reduce_add_sync(0xffffffffu, cnt);
+    const unsigned e = (unsigned)((float)tot * per);            // estimated evaluated samples
+    return min(kBuckets - 1, 31 - __clz((int)(e + 1u)));
+}
+
 template <int KF>
 __device__ __forceinline__ void emit_segment(const DevScene& S, int g, const double o[3], const double d[3],
                                              double t_a, double t_b, int64_t r, int64_t ray,
@@ -193,6 +301,7 @@ __device__ __forceinline__ void emit_segment(const DevScene& S, int g, const dou
                                              unsigned& reg_mask) {
     Segment sg;
     if (!make_segment(S, g, o, d, t_a, t_b, sg)) return;   // zero length: dropped
+
     if (KF & KF_SEGS) {
         if (nseg < ta.max_per_ray) {
             merf_segment rec;
@@ -240,7 +349,15 @@ __global__ void __launch_bounds__(kSetupThreads) setup_kernel(DevScene S, RaySou
                 t_near = rs.cb.cam[view].t_near;
             }
         }
-        if (valid) {
+        if (valid && (KF & KF_SPH)) {
+            // spherical variant: no segments; the march steps the curve from (o, d, t_near)
+            int4* p = ws.seg + (r * kMaxSeg) * 2;
+            p[0] = make_int4(__float_as_int((float)o[0]), __float_as_int((float)o[1]), __float_as_int((float)o[2]),
+                             __float_as_int((float)t_near));
+            p[1] = make_int4(__float_as_int((float)d[0]), __float_as_int((float)d[1]), __float_as_int((float)d[2]), 0);
+            nseg = 1;
+            reg_mask = 1u;
+        } else if (valid) {
             double cand[12];
             boundary_candidates(o, d, t_near, cand);
             // Walk the sorted boundaries (staged in this thread's shared-memory row: dynamic
@@ -281,6 +398,15 @@ __global__ void __launch_bounds__(kSetupThreads) setup_kernel(DevScene S, RaySou
         if (r < rs.n) ta.counts[ray] = nseg;
     } else if (r < rs.n) {
         ws.nseg[r] = (uint8_t)min(nseg, kMaxSeg);
+    }
+    if (!(KF & (KF_SEGS | KF_TRACE | KF_SPH)) && ws.tile_list) {
+        // one 32-ray tile per warp (chunks are tile aligned): file it under its cost bucket
+        __syncwarp();                                  // the centre ray's segments are written
+        const int b = tile_cost_bucket(S, ws, r, rs.n);
+        if ((threadIdx.x & 31) == 0 && r < rs.n) {
+            const unsigned slot = atomicAdd(ws.bucket_cnt + b, 1u);
+            ws.tile_list[(int64_t)b * ws.n_tiles + slot] = (int)(r >> 5);
+        }
     }
     if (KF & KF_COUNT) {
         add_stat(stats, 0, valid ? 1 : 0);
@@ -504,6 +630,9 @@ __global__ void __launch_bounds__(kMarchThreads, MERF_MARCH_MINB) march_kernel(D
     const int sf = Geo<KF>::sf(S);
     const uint32_t* occ_f = S.occ_fin;
     const bool early_term = !(rflags & MERF_NO_EARLY_TERM);
+    // spherical variant: step cap and stop radius of the oracle's curve march (2 - Delta)
+    const int sph_kmax = (KF & KF_SPH) ? (int)(8.0 / S.step) + 8 : 0;
+    const float sph_stop = (KF & KF_SPH) ? 2.f - S.step_f : 0.f;
 
     // per-lane ray state
     int ray = -1;                      // chunk-local ray index (chunks < 2^31 rays)
@@ -516,6 +645,10 @@ __global__ void __launch_bounds__(kMarchThreads, MERF_MARCH_MINB) march_kernel(D
     st.F[0] = st.F[1] = st.F[2] = st.F[3] = 0.f;
     int c_eval = 0, c_donly = 0, c_skip = 0, c_miss = 0, c_rounds = 0, c_steps = 0, c_lanes = 0;
 
+    if (KF & KF_COUNT) {
+        if (lane == 0) atomicMin(stats + 16, gtime());
+    }
+
     auto finish = [&]() {
         store_accum(ws.accum + (int64_t)ray * 2, st);
         if (KF & KF_TRACE) ta.counts[ray] = n_eval;
@@ -526,10 +659,25 @@ __global__ void __launch_bounds__(kMarchThreads, MERF_MARCH_MINB) march_kernel(D
         // ---------------- tile scheduling: a new tile of 32 rays when the warp is empty -------
         unsigned act = __ballot_sync(FULL, ray >= 0);
         if (act == 0) {
-            unsigned base = 0;
-            if (lane == 0) base = atomicAdd(ws.queue, 32u);
-            base = __shfl_sync(FULL, base, 0);
-            if ((int64_t)base >= n_rays) break;
+            int tile = 0;
+            if (lane == 0) {
+                int t = (int)atomicAdd(ws.queue, 1u);
+                tile = t;
+                if (ws.tile_list && t < ws.n_tiles) {
+                    // the cost-ordered lists, most expensive bucket first
+                    for (int b = kBuckets - 1; b >= 0; b--) {
+                        const int c = (int)__ldg(ws.bucket_cnt + b);
+                        if (t < c) { tile = __ldg(ws.tile_list + (int64_t)b * ws.n_tiles + t); break; }
+                        t -= c;
+                    }
+                }
+            }
+            tile = __shfl_sync(FULL, tile, 0);
+            const unsigned base = (unsigned)tile << 5;
+            if (tile >= ws.n_tiles) {
+                if ((KF & KF_COUNT) && lane == 0) atomicMin(stats + 17, gtime());
+                break;
+            }
             if ((int64_t)base + lane < n_rays) {
                 ray = (int)base + lane;
                 ns = ws.nseg[ray];
@@ -559,6 +707,38 @@ __global__ void __launch_bounds__(kMarchThreads, MERF_MARCH_MINB) march_kernel(D
         int Qx = 0, Qy = 0, Qz = 0, fcell = 0;
         // one traversal step of a lane that wants a sample
         auto step = [&]() {
+            if (KF & KF_SPH) {
+                // Eq. 4 contraction: sample k at t, then t += Delta / sigma(t)
+                // (reading S1) in fp32; every sample is tested against the finest level -- lines
+                // map to curves, so there is no AABB skip.  qa = (o, t), uu = d (fp32 bits).
+                if (ns == 0 || k >= sph_kmax) { finish(); return; }
+                const float t = __int_as_float(qa.w);
+                const float dx = __int_as_float(uu.x), dy = __int_as_float(uu.y), dz = __int_as_float(uu.z);
+                const float x0 = fmaf(t, dx, __int_as_float(qa.x)), x1 = fmaf(t, dy, __int_as_float(qa.y)),
+                            x2 = fmaf(t, dz, __int_as_float(qa.z));
+                const float r2 = fmaf(x0, x0, fmaf(x1, x1, x2 * x2));
+                const float r = sqrtf(r2);
+                float cr = r, sc = 1.f, speed = 1.f;
+                if (r > 1.f) {
+                    const float inv = __fdividef(1.f, r);
+                    cr = 2.f - inv;
+                    sc = cr * inv;
+                    const float dr = fmaf(dx, x0, fmaf(dy, x1, dz * x2)) * inv;   // radial speed
+                    const float inv2 = inv * inv;
+                    const float ra = dr * inv2, rb = fmaf(2.f, r, -1.f) * inv2;
+                    const float perp = fmaxf(fmaf(-dr, dr, 1.f), 0.f);
+                    speed = sqrtf(fmaf(ra, ra, rb * rb * perp));
+                }
+                if (cr >= sph_stop) { finish(); return; }
+                const float q = sc * (float)kOne;
+                Qx = __float2int_rn(x0 * q) + kTwoI;
+                Qy = __float2int_rn(x1 * q) + kTwoI;
+                Qz = __float2int_rn(x2 * q) + kTwoI;
+                qa.w = __float_as_int(fmaf(S.step_f, __fdividef(1.f, speed), t));
+                k++;
+                if (occ_bit(occ_f, occ_cell(Qx, sf, Nf), occ_cell(Qy, sf, Nf), occ_cell(Qz, sf, Nf), Nf)) found = true;
+                return;
+            }
             if (k >= qa.w) {                                  // segment exhausted
                 j++;
                 if (j >= ns) { finish(); return; }
@@ -682,11 +862,12 @@ __global__ void __launch_bounds__(kMarchThreads, MERF_MARCH_MINB) march_kernel(D
                 }
             }
             n_eval++;
-            k++;
+            if (!(KF & KF_SPH)) k++;                          // (the curve step advanced k already)
             if (early_term && st.T < S.t_min) finish();
         }
     }
     if (KF & KF_COUNT) {
+        if (lane == 0) atomicMax(stats + 18, gtime());
         add_stat(stats, 2, c_eval);
         add_stat(stats, 3, c_donly);
         add_stat(stats, 4, c_skip);

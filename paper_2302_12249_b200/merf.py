@@ -21,6 +21,7 @@ LIB_PATH = os.environ.get("MERF_LIB") or os.path.join(_HERE, "libmerf.so")
 MERF_OK, MERF_EINVAL, MERF_ENOMEM, MERF_ECUDA, MERF_ENCCL, MERF_EMISMATCH, MERF_EIO = range(7)
 MERF_RGB_F32, MERF_RGBA_U8 = 0, 1
 MERF_NO_EARLY_TERM, MERF_COUNTERS, MERF_DENSE, MERF_TIMED, MERF_SPHERICAL, MERF_MLP_FFMA = 1, 2, 4, 8, 16, 32
+MERF_SPH_PERSISTENT = 64
 MAX_LEVELS = 4
 
 _STATUS = {1: "MERF_EINVAL", 2: "MERF_ENOMEM", 3: "MERF_ECUDA", 4: "MERF_ENCCL", 5: "MERF_EMISMATCH", 6: "MERF_EIO"}
@@ -55,7 +56,7 @@ class merf_stats(C.Structure):
     _fields_ = [("rays", C.c_int64), ("segments", C.c_int64), ("evaluated", C.c_int64),
                 ("density_only", C.c_int64), ("skips", C.c_int64), ("missing_blocks", C.c_int64),
                 ("region_segments", C.c_int64 * 7), ("march_rounds", C.c_int64), ("march_steps", C.c_int64),
-                ("march_lane_rounds", C.c_int64)]
+                ("march_lane_rounds", C.c_int64), ("march_busy_ns", C.c_int64), ("march_tail_ns", C.c_int64)]
 
     def as_dict(self):
         d = {k: int(getattr(self, k)) for k, _ in self._fields_ if k != "region_segments"}

@@ -43,9 +43,12 @@ def main():
             torch.cuda.synchronize()
             kt = M.merf_kernel_times_get(s.handle, reset=True)
             call = e0.elapsed_time(e1) / a.reps
+            stc = M.merf_render(s.handle, cams, 1920, 1080, out, fmt=M.MERF_RGBA_U8, stream=st, stats=True)
             ln = {"mode": mode, "views": n, "call_ms": call, "call_ms_per_view": call / n,
                   "setup_ms_per_view": kt["setup_ms"] / a.reps / n, "march_ms_per_view": kt["march_ms"] / a.reps / n,
-                  "shade_ms_per_view": kt["shade_ms"] / a.reps / n}
+                  "shade_ms_per_view": kt["shade_ms"] / a.reps / n,
+                  "march_busy_ms": stc["march_busy_ns"] / 1e6, "march_tail_ms": stc["march_tail_ns"] / 1e6,
+                  "note": "busy/tail from the counter instance: first warp start -> tile queue dry -> last exit"}
             print(json.dumps(ln), flush=True)
             lines.append(ln)
     s.close()
