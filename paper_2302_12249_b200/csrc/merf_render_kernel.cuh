@@ -630,7 +630,7 @@ __global__ void __launch_bounds__(kMarchThreads, MERF_MARCH_MINB) march_kernel(D
     const int sf = Geo<KF>::sf(S);
     const uint32_t* occ_f = S.occ_fin;
     const bool early_term = !(rflags & MERF_NO_EARLY_TERM);
-    // spherical variant: step cap and stop radius of the oracle's curve march (2 - Delta)
+    // spherical variant: step cap and stop radius of the curve march (reading S1: k < 8 / Delta + 8, stop at radius 2 - Delta)
     const int sph_kmax = (KF & KF_SPH) ? (int)(8.0 / S.step) + 8 : 0;
     const float sph_stop = (KF & KF_SPH) ? 2.f - S.step_f : 0.f;
 
