@@ -8,6 +8,7 @@ python bench.py --steps 5 --no-cpu-baseline --no-e2e --dense > gpurun_out/abl_de
 MERF_NO_SKIPTAB=1 python bench.py --steps 10 --no-cpu-baseline --no-e2e > gpurun_out/abl_noskiptab.json 2>/dev/null
 python bench.py --steps 10 --no-cpu-baseline --no-e2e --mlp-ffma > gpurun_out/abl_mlpffma.json 2>/dev/null
 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --spherical > gpurun_out/abl_spherical.json 2>/dev/null
+python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --spherical --sph-persistent > gpurun_out/abl_spherical_persistent.json 2>/dev/null
 python tools/bench_progressive.py --out gpurun_out/abl_progressive.jsonl > gpurun_out/abl_progressive.log 2>&1
 python tools/bench_qat.py --out gpurun_out/abl_qat.jsonl > gpurun_out/abl_qat.log 2>&1
 python tools/bench_bake.py > gpurun_out/abl_bake.log 2>&1
