@@ -350,12 +350,13 @@ def main():
             n_seg += st["segments"]
             region_segs = [a + b for a, b in zip(region_segs, st["region_segments"])]
     rays_per_step = V * W_IMG * H_IMG
-    ws = M.merf_render_workspace_bytes(scene.handle, V, W_IMG, H_IMG)
+    ws = M.merf_render_workspace_bytes(scene.handle, batches[args.warmup], W_IMG, H_IMG)
     vram = {"scene_device_bytes": info["device_bytes"], "baked_arrays_bytes": int(sc.nbytes()),
             "render_workspace_bytes": ws["bytes"], "workspace_bytes_per_ray": ws["bytes_per_ray"],
             "frame_buffers_bytes": 2 * V * H_IMG * W_IMG * 4,
             "note": "scene = every device layout built at upload (DESIGN 5); workspace = one merf_render "
-                    "chunk (7 segment slots + accumulators per ray)"}
+                    "chunk (4 segment slots per ray for cameras inside the core, else 7; accumulators; "
+                    "tile lists)"}
 
     gathered = [torch.cuda.Event() for _ in range(2)]   # buffer b's last gather finished
 

@@ -199,13 +199,14 @@ merf_status merf_render(const merf_scene *scene, const merf_camera *cams, int32_
                         void *stream, merf_stats *stats);
 
 /*
- * Device workspace a merf_render(scene, n_cams views of W x H) call allocates from the
- * stream-ordered pool for its chunk of rays (segments, accumulators, queue): *bytes, and the
- * rays of one chunk in *rays_per_chunk (optional).  Host-only arithmetic, no device work.
- * Errors: MERF_EINVAL.
+ * Device workspace a merf_render(scene, cams, n_cams views of W x H) call allocates from the
+ * stream-ordered pool for its chunk of rays (segments, accumulators, queue, tile lists):
+ * *bytes, and the rays of one chunk in *rays_per_chunk (optional).  cams [host] may be NULL
+ * (worst case: 7 segment slots per ray; cameras whose origins are all in the core need 4).
+ * Host-only arithmetic, no device work.  Errors: MERF_EINVAL.
  */
-merf_status merf_render_workspace_bytes(const merf_scene *scene, int32_t n_cams, int32_t W, int32_t H,
-                                        int64_t *bytes, int64_t *rays_per_chunk);
+merf_status merf_render_workspace_bytes(const merf_scene *scene, const merf_camera *cams, int32_t n_cams,
+                                        int32_t W, int32_t H, int64_t *bytes, int64_t *rays_per_chunk);
 
 /* Collect (and, if reset != 0, clear) the MERF_TIMED kernel times of `scene`. */
 merf_status merf_kernel_times_get(merf_scene *scene, merf_kernel_times *out, int32_t reset);

@@ -464,9 +464,20 @@ static size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 // workspace bytes of a chunk of n rays (shared with
 // merf_render_workspace_bytes so that the reported figure is the allocated one)
 static size_t ws_tiles(int64_t n) { return (size_t)((n + 31) / 32); }
-static size_t ws_bytes(int64_t n) {
-    return align256((size_t)n * kMaxSeg * 32) + align256((size_t)n) + align256((size_t)n * 32) + 256
+static size_t ws_bytes(int64_t n, int slots) {
+    return align256((size_t)n * slots * 32) + align256((size_t)n) + align256((size_t)n * 32) + 256
            + align256(ws_tiles(n) * kBuckets * 4) + 256;
+}
+
+// segment slots per ray for a chunk of these cameras: kMaxSegCore if every origin is in the
+// core (||o||_inf <= 1, o = the c2w translation), else kMaxSeg (merf_device.cuh)
+static int seg_slots_for(const merf_camera* cams, int n) {
+    if (!cams) return kMaxSeg;
+    for (int i = 0; i < n; i++) {
+        const double* m = cams[i].c2w;
+        if (!(std::fabs(m[3]) <= 1.0 && std::fabs(m[7]) <= 1.0 && std::fabs(m[11]) <= 1.0)) return kMaxSeg;
+    }
+    return kMaxSegCore;
 }
 
 // Tile dispatch order.  Cost-ordered (longest first, Workspace::tile_list) for launches of at
@@ -477,6 +488,10 @@ static size_t ws_bytes(int64_t n) {
 // share of the launch (1-4 views: 1.8 % to 6 % faster per view); at 16 views it is a 2 % loss.
 // MERF_TILE_ORDER=raster / cost forces either order (A/B).
 static const int kLptMaxViews = 4;
+static bool fused_mlp() {
+    static const bool v = [] { const char* e = getenv("MERF_FUSED_MLP"); return e && e[0] == '1'; }();
+    return v;
+}
 static int tile_order_override() {                   // 0 = policy, 1 = raster, 2 = cost
     static const int v = [] {
         const char* e = getenv("MERF_TILE_ORDER");
@@ -492,13 +507,14 @@ static bool cost_order(int views_per_chunk) {
     return o == 2 || (o == 0 && views_per_chunk <= kLptMaxViews);
 }
 
-static merf_status ws_alloc(int64_t n, cudaStream_t st, Workspace& ws, void** base) {
-    const size_t seg = align256((size_t)n * kMaxSeg * 32);
+static merf_status ws_alloc(int64_t n, cudaStream_t st, Workspace& ws, void** base, int slots = kMaxSeg) {
+    const size_t seg = align256((size_t)n * slots * 32);
+    ws.seg_slots = slots;
     const size_t ns = align256((size_t)n);
     const size_t acc = align256((size_t)n * 32);
-    CUDA_TRY(cudaMallocAsync(base, ws_bytes(n), st));
+    CUDA_TRY(cudaMallocAsync(base, ws_bytes(n, slots), st));
     static const bool poison = getenv("MERF_DEBUG_POISON") != nullptr;   // debug: NaN-fill
-    if (poison) CUDA_TRY(cudaMemsetAsync(*base, 0xFF, ws_bytes(n), st));
+    if (poison) CUDA_TRY(cudaMemsetAsync(*base, 0xFF, ws_bytes(n, slots), st));
     char* b = (char*)*base;
     ws.seg = (int4*)b;
     ws.nseg = (uint8_t*)(b + seg);
@@ -555,7 +571,7 @@ static cudaError_t call_setup(void* p) {
 }
 static cudaError_t call_march(void* p) {
     ChunkCall* c = (ChunkCall*)p;
-    return launch_march(c->kf_march, c->s->dev, c->rs->n, *c->ws, c->flags, *c->ta, c->d_stats, c->st);
+    return launch_march(c->kf_march, c->s->dev, c->rs->n, *c->ws, c->flags, *c->ta, c->d_stats, c->st, *c->rs, c->out);
 }
 static cudaError_t call_march_sph(void* p) {
     ChunkCall* c = (ChunkCall*)p;
@@ -573,6 +589,14 @@ static merf_status run_chunk(const merf_scene* s, int kf_setup, int kf_march, in
                              const TraceArgs& ta, unsigned long long* d_stats, cudaStream_t st) {
     Workspace ws = ws_in;
     ws.n_tiles = (int)ws_tiles(rs.n);                 // this chunk's tiles
+    // fused deferred-MLP epilogue in the march (KF_FUSED): camera rays of the production
+    // instance, not the progressive preview fill nor the FFMA ablation (MERF_FUSED_MLP=0/1)
+    if (fused_mlp() && kf_march >= 0 && kf_shade >= 0 && !(kf_march & (KF_DENSE | KF_TRACE)) &&
+        !(kf_setup & (KF_RAYS | KF_TRACE | KF_SEGS)) && !rs.fill && !(flags & (MERF_MLP_FFMA | MERF_SPHERICAL)) &&
+        fused_march_ok(s->dev) && !(kf_march & KF_COUNT)) {
+        kf_march = KF_FUSED | (kf_shade & KF_U8);
+        kf_shade = -1;
+    }
     if ((flags & MERF_SPHERICAL) && (flags & MERF_SPH_PERSISTENT) && !(kf_setup & (KF_TRACE | KF_SEGS))) {
         kf_setup |= KF_SPH;                // like-for-like: the persistent pipeline, fp32 curve steps
         if (kf_march >= 0) kf_march = KF_SPH | (kf_march & KF_COUNT);
@@ -662,7 +686,7 @@ static merf_status render_frames(const merf_scene* s, const merf_camera* cams, i
     if (vpc > n_cams) vpc = n_cams;
     Workspace ws;
     void* base = nullptr;
-    merf_status e = ws_alloc(rays_per_view * vpc, st, ws, &base);
+    merf_status e = ws_alloc(rays_per_view * vpc, st, ws, &base, seg_slots_for(cams, n_cams));
     if (e) return e;
     if (!cost_order(vpc)) ws.tile_list = nullptr;
     const bool count = d_stats != nullptr;
@@ -709,8 +733,8 @@ extern "C" merf_status merf_render(const merf_scene* s, const merf_camera* cams,
     return MERF_OK;
 }
 
-extern "C" merf_status merf_render_workspace_bytes(const merf_scene* s, int32_t n_cams, int32_t W, int32_t H,
-                                                   int64_t* bytes, int64_t* rays_per_chunk) {
+extern "C" merf_status merf_render_workspace_bytes(const merf_scene* s, const merf_camera* cams, int32_t n_cams,
+                                                   int32_t W, int32_t H, int64_t* bytes, int64_t* rays_per_chunk) {
     if (!s || !bytes || n_cams <= 0 || W <= 0 || H <= 0) return fail(MERF_EINVAL, "bad arguments");
     const int64_t tiles = (int64_t)((W + kTileW - 1) / kTileW) * ((H + kTileH - 1) / kTileH);
     const int64_t rays_per_view = tiles * 32;
@@ -718,7 +742,7 @@ extern "C" merf_status merf_render_workspace_bytes(const merf_scene* s, int32_t 
     int64_t vpc = kChunkRays * cv / kViewsPerChunk / rays_per_view;
     vpc = vpc < 1 ? 1 : (vpc > cv ? cv : vpc);
     if (vpc > n_cams) vpc = n_cams;
-    *bytes = (int64_t)ws_bytes(rays_per_view * vpc);
+    *bytes = (int64_t)ws_bytes(rays_per_view * vpc, seg_slots_for(cams, n_cams));
     if (rays_per_chunk) *rays_per_chunk = rays_per_view * vpc;
     return MERF_OK;
 }

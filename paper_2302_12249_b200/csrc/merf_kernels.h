@@ -14,7 +14,11 @@ struct TraceArgs;
 cudaError_t launch_setup(int kf, const DevScene& S, const RaySource& rs, const Workspace& ws,
                          const TraceArgs& ta, unsigned long long* stats, cudaStream_t st);
 cudaError_t launch_march(int kf, const DevScene& S, int64_t n, const Workspace& ws, uint32_t rflags,
-                         const TraceArgs& ta, unsigned long long* stats, cudaStream_t st);
+                         const TraceArgs& ta, unsigned long long* stats, cudaStream_t st,
+                         const RaySource& rs, void* out);
+// the fused-epilogue march instance applies to this scene (paper geometry, all sources, skip
+// table, tensor-core MLP table)
+bool fused_march_ok(const DevScene& S);
 cudaError_t launch_march_sph(int kf, const DevScene& S, const RaySource& rs, const Workspace& ws,
                              uint32_t rflags, const TraceArgs& ta, unsigned long long* stats, cudaStream_t st);
 cudaError_t launch_shade(int kf, const DevScene& S, const RaySource& rs, const Workspace& ws, void* out,

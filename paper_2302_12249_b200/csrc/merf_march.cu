@@ -20,7 +20,8 @@ static MarchTune march_tune() {
 
 template <int KF>
 static cudaError_t march_v(const DevScene& S, int64_t n, const Workspace& ws, uint32_t rflags,
-                           const TraceArgs& ta, unsigned long long* stats, cudaStream_t st) {
+                           const TraceArgs& ta, unsigned long long* stats, cudaStream_t st,
+                           const RaySource& rs, void* out) {
     if (n <= 0) return cudaSuccess;
     // persistent grid: resident CTAs x SMs, cached per variant and per device (the caller's
     // entry point has made the scene's device current)
@@ -39,7 +40,7 @@ static cudaError_t march_v(const DevScene& S, int64_t n, const Workspace& ws, ui
     int grid = (int)(need < blocks ? need : blocks);
     cudaError_t e = cudaMemsetAsync(ws.queue, 0, sizeof(unsigned int), st);
     if (e != cudaSuccess) return e;
-    march_kernel<KF><<<grid, kMarchThreads, 0, st>>>(S, n, ws, rflags, ta, stats, march_tune());
+    march_kernel<KF><<<grid, kMarchThreads, 0, st>>>(S, n, ws, rflags, ta, stats, march_tune(), rs, out);
     return cudaGetLastError();
 }
 
@@ -76,48 +77,57 @@ static bool paper_geometry(const DevScene& S) {
     return S.L == kPaperL && S.R == kPaperR && S.n_fin == kPaperNf && !env_flag("MERF_NO_PAPER");
 }
 
+bool fused_march_ok(const DevScene& S) {
+    return S.n_src == 4 && use_skiptab(S) && paper_geometry(S) && S.mlp_frag != nullptr;
+}
+
 cudaError_t launch_march(int kf, const DevScene& S, int64_t n, const Workspace& ws, uint32_t rflags,
-                         const TraceArgs& ta, unsigned long long* stats, cudaStream_t st) {
+                         const TraceArgs& ta, unsigned long long* stats, cudaStream_t st,
+                         const RaySource& rs, void* out) {
+    if (kf & KF_FUSED) {                              // production + fused MLP epilogue (paper geometry)
+        if (kf & KF_U8) return march_v<KF_ALLSRC | KF_SKIPTAB | KF_PAPER | KF_FUSED | KF_U8>(S, n, ws, rflags, ta, stats, st, rs, out);
+        return march_v<KF_ALLSRC | KF_SKIPTAB | KF_PAPER | KF_FUSED>(S, n, ws, rflags, ta, stats, st, rs, out);
+    }
     if (kf & KF_SPH) {                                // NEXT-2 like-for-like variant
         if (S.n_src == 4 && paper_geometry(S)) {
-            if (kf & KF_COUNT) return march_v<KF_SPH | KF_ALLSRC | KF_PAPER | KF_COUNT>(S, n, ws, rflags, ta, stats, st);
-            return march_v<KF_SPH | KF_ALLSRC | KF_PAPER>(S, n, ws, rflags, ta, stats, st);
+            if (kf & KF_COUNT) return march_v<KF_SPH | KF_ALLSRC | KF_PAPER | KF_COUNT>(S, n, ws, rflags, ta, stats, st, rs, out);
+            return march_v<KF_SPH | KF_ALLSRC | KF_PAPER>(S, n, ws, rflags, ta, stats, st, rs, out);
         }
-        if (kf & KF_COUNT) return march_v<KF_SPH | KF_COUNT>(S, n, ws, rflags, ta, stats, st);
-        return march_v<KF_SPH>(S, n, ws, rflags, ta, stats, st);
+        if (kf & KF_COUNT) return march_v<KF_SPH | KF_COUNT>(S, n, ws, rflags, ta, stats, st, rs, out);
+        return march_v<KF_SPH>(S, n, ws, rflags, ta, stats, st, rs, out);
     }
     const bool tab = use_skiptab(S);
     if (S.n_src == 4 && !(kf & (KF_TRACE | KF_DENSE))) {    // production variants
         if (tab) {
             if (paper_geometry(S)) {
-                if (kf & KF_COUNT) return march_v<KF_ALLSRC | KF_SKIPTAB | KF_PAPER | KF_COUNT>(S, n, ws, rflags, ta, stats, st);
-                return march_v<KF_ALLSRC | KF_SKIPTAB | KF_PAPER>(S, n, ws, rflags, ta, stats, st);
+                if (kf & KF_COUNT) return march_v<KF_ALLSRC | KF_SKIPTAB | KF_PAPER | KF_COUNT>(S, n, ws, rflags, ta, stats, st, rs, out);
+                return march_v<KF_ALLSRC | KF_SKIPTAB | KF_PAPER>(S, n, ws, rflags, ta, stats, st, rs, out);
             }
-            if (kf & KF_COUNT) return march_v<KF_ALLSRC | KF_SKIPTAB | KF_COUNT>(S, n, ws, rflags, ta, stats, st);
-            return march_v<KF_ALLSRC | KF_SKIPTAB>(S, n, ws, rflags, ta, stats, st);
+            if (kf & KF_COUNT) return march_v<KF_ALLSRC | KF_SKIPTAB | KF_COUNT>(S, n, ws, rflags, ta, stats, st, rs, out);
+            return march_v<KF_ALLSRC | KF_SKIPTAB>(S, n, ws, rflags, ta, stats, st, rs, out);
         }
-        if (kf & KF_COUNT) return march_v<KF_ALLSRC | KF_COUNT>(S, n, ws, rflags, ta, stats, st);
-        return march_v<KF_ALLSRC>(S, n, ws, rflags, ta, stats, st);
+        if (kf & KF_COUNT) return march_v<KF_ALLSRC | KF_COUNT>(S, n, ws, rflags, ta, stats, st, rs, out);
+        return march_v<KF_ALLSRC>(S, n, ws, rflags, ta, stats, st, rs, out);
     }
     // traces: the production instances (the ones merf_render times) plus the trace writes, so
     // the traversal and gather code of the timed kernel is what the bit-exact trace tests check
     if (tab && S.n_src == 4 && (kf & (KF_TRACE | KF_DENSE | KF_COUNT)) == KF_TRACE) {
-        if (paper_geometry(S)) return march_v<KF_TRACE | KF_ALLSRC | KF_SKIPTAB | KF_PAPER>(S, n, ws, rflags, ta, stats, st);
-        return march_v<KF_TRACE | KF_ALLSRC | KF_SKIPTAB>(S, n, ws, rflags, ta, stats, st);
+        if (paper_geometry(S)) return march_v<KF_TRACE | KF_ALLSRC | KF_SKIPTAB | KF_PAPER>(S, n, ws, rflags, ta, stats, st, rs, out);
+        return march_v<KF_TRACE | KF_ALLSRC | KF_SKIPTAB>(S, n, ws, rflags, ta, stats, st, rs, out);
     }
     if (tab && (kf & (KF_TRACE | KF_DENSE | KF_COUNT)) == KF_TRACE)
-        return march_v<KF_TRACE | KF_SKIPTAB>(S, n, ws, rflags, ta, stats, st);
+        return march_v<KF_TRACE | KF_SKIPTAB>(S, n, ws, rflags, ta, stats, st, rs, out);
     if (tab && (kf & (KF_TRACE | KF_DENSE | KF_COUNT)) == 0)
-        return march_v<KF_SKIPTAB>(S, n, ws, rflags, ta, stats, st);
+        return march_v<KF_SKIPTAB>(S, n, ws, rflags, ta, stats, st, rs, out);
     if (tab && (kf & (KF_TRACE | KF_DENSE | KF_COUNT)) == KF_COUNT)
-        return march_v<KF_SKIPTAB | KF_COUNT>(S, n, ws, rflags, ta, stats, st);
+        return march_v<KF_SKIPTAB | KF_COUNT>(S, n, ws, rflags, ta, stats, st, rs, out);
     switch (kf & (KF_TRACE | KF_DENSE | KF_COUNT)) {
-        case 0: return march_v<0>(S, n, ws, rflags, ta, stats, st);
-        case KF_COUNT: return march_v<KF_COUNT>(S, n, ws, rflags, ta, stats, st);
-        case KF_DENSE: return march_v<KF_DENSE>(S, n, ws, rflags, ta, stats, st);
-        case KF_DENSE | KF_COUNT: return march_v<KF_DENSE | KF_COUNT>(S, n, ws, rflags, ta, stats, st);
-        case KF_TRACE: return march_v<KF_TRACE>(S, n, ws, rflags, ta, stats, st);
-        case KF_TRACE | KF_DENSE: return march_v<KF_TRACE | KF_DENSE>(S, n, ws, rflags, ta, stats, st);
+        case 0: return march_v<0>(S, n, ws, rflags, ta, stats, st, rs, out);
+        case KF_COUNT: return march_v<KF_COUNT>(S, n, ws, rflags, ta, stats, st, rs, out);
+        case KF_DENSE: return march_v<KF_DENSE>(S, n, ws, rflags, ta, stats, st, rs, out);
+        case KF_DENSE | KF_COUNT: return march_v<KF_DENSE | KF_COUNT>(S, n, ws, rflags, ta, stats, st, rs, out);
+        case KF_TRACE: return march_v<KF_TRACE>(S, n, ws, rflags, ta, stats, st, rs, out);
+        case KF_TRACE | KF_DENSE: return march_v<KF_TRACE | KF_DENSE>(S, n, ws, rflags, ta, stats, st, rs, out);
         default: return cudaErrorInvalidValue;
     }
 }

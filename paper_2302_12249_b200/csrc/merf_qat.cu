@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(128) qat_fwd_kernel(RaySource rs, Workspace ws
     bool over = false;
     const int ns = ws.nseg[r];
     for (int j = 0; j < ns; j++) {
-        const int4 qa = ws.seg[(r * kMaxSeg + j) * 2], uu = ws.seg[(r * kMaxSeg + j) * 2 + 1];
+        const int4 qa = ws.seg[(r * ws.seg_slots + j) * 2], uu = ws.seg[(r * ws.seg_slots + j) * 2 + 1];
         for (int k = 0; k < qa.w; k++) {
             const int Qx = qa.x + k * uu.x, Qy = qa.y + k * uu.y, Qz = qa.z + k * uu.z;
             if (!occ_bit(A.occf, occ_cell(Qx, A.sf, A.Nf), occ_cell(Qy, A.sf, A.Nf), occ_cell(Qz, A.sf, A.Nf), A.Nf))

@@ -23,6 +23,7 @@
 
 #include "merf_device.cuh"
 #include "merf_kernels.h"
+#include "merf_mma.cuh"
 
 namespace merf {
 
@@ -38,6 +39,8 @@ enum : int {
     KF_PAPER = 256,     // the paper's default resolutions as compile-time constants (below)
     KF_SPH = 512,       // NEXT-2 like-for-like: spherical contraction, fp32 curve stepping in the
                         // persistent tile-scheduled march (MERF_SPHERICAL | MERF_SPH_PERSISTENT)
+    KF_FUSED = 1024,    // the deferred MLP (tensor cores) and the output store run in the march
+                        // at each tile's end: no shade kernel, no accumulator round trip
 };
 
 // The paper's default scene geometry (L = 512, R = 2048; finest occupancy level
@@ -176,7 +179,8 @@ __device__ __forceinline__ int64_t out_index(const RaySource& rs, int view, int 
 constexpr int kBuckets = 8;
 
 struct Workspace {
-    int4* seg;                   // [n][kMaxSeg][2]: (Qa.xyz, K), (U.xyz, region)
+    int4* seg;                   // [n][seg_slots][2]: (Qa.xyz, K), (U.xyz, region)
+    int seg_slots;               // segment slots per ray: kMaxSeg, or kMaxSegCore (see below)
     uint8_t* nseg;               // [n]
     float4* accum;               // [n][2]: (C_d.rgb, T), (F0..F3)
     unsigned int* queue;         // tile counter of the persistent march
@@ -263,7 +267,7 @@ __device__ __forceinline__ int tile_cost_bucket(const DevScene& S, const Workspa
     const int64_t rc = (r & ~(int64_t)31) + kCostLane;
     int ns = 0;
     if (rc < n) ns = ws.nseg[rc];
-    const int4* sp = ws.seg + rc * kMaxSeg * 2;
+    const int4* sp = ws.seg + rc * ws.seg_slots * 2;
     int Ktot = 0;
     for (int j = 0; j < ns; j++) Ktot += sp[2 * j].w;            // uniform loop (same ray)
     float od[2] = {-1.f, -1.f};
@@ -313,8 +317,8 @@ __device__ __forceinline__ void emit_segment(const DevScene& S, int g, const dou
             rec.region = sg.region;
             ta.segs[ray * ta.max_per_ray + nseg] = rec;
         }
-    } else if (nseg < kMaxSeg) {
-        int4* p = ws.seg + (r * kMaxSeg + nseg) * 2;
+    } else if (nseg < ws.seg_slots) {
+        int4* p = ws.seg + (r * ws.seg_slots + nseg) * 2;
         p[0] = make_int4(sg.Qa[0] + kTwoI, sg.Qa[1] + kTwoI, sg.Qa[2] + kTwoI, sg.K);   // biased origin
         p[1] = make_int4(sg.U[0], sg.U[1], sg.U[2], sg.region);
     }
@@ -323,7 +327,7 @@ __device__ __forceinline__ void emit_segment(const DevScene& S, int g, const dou
 }
 
 template <int KF>
-__global__ void __launch_bounds__(kSetupThreads) setup_kernel(DevScene S, RaySource rs, Workspace ws,
+__global__ void __launch_bounds__(kSetupThreads, 7) setup_kernel(DevScene S, RaySource rs, Workspace ws,
                                                               TraceArgs ta, unsigned long long* stats) {
     __shared__ double s_cand[kSetupThreads][13];   // 13: odd stride, conflict-free rows
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // index within chunk
@@ -351,7 +355,7 @@ __global__ void __launch_bounds__(kSetupThreads) setup_kernel(DevScene S, RaySou
         }
         if (valid && (KF & KF_SPH)) {
             // spherical variant: no segments; the march steps the curve from (o, d, t_near)
-            int4* p = ws.seg + (r * kMaxSeg) * 2;
+            int4* p = ws.seg + (r * ws.seg_slots) * 2;
             p[0] = make_int4(__float_as_int((float)o[0]), __float_as_int((float)o[1]), __float_as_int((float)o[2]),
                              __float_as_int((float)t_near));
             p[1] = make_int4(__float_as_int((float)d[0]), __float_as_int((float)d[1]), __float_as_int((float)d[2]), 0);
@@ -397,7 +401,8 @@ __global__ void __launch_bounds__(kSetupThreads) setup_kernel(DevScene S, RaySou
     if (KF & KF_SEGS) {
         if (r < rs.n) ta.counts[ray] = nseg;
     } else if (r < rs.n) {
-        ws.nseg[r] = (uint8_t)min(nseg, kMaxSeg);
+        MERF_CHECK(nseg <= ws.seg_slots);        // kMaxSegCore bound (proof at kMaxSegCore)
+        ws.nseg[r] = (uint8_t)min(nseg, ws.seg_slots);
     }
     if (!(KF & (KF_SEGS | KF_TRACE | KF_SPH)) && ws.tile_list) {
         // one 32-ray tile per warp (chunks are tile aligned): file it under its cost bucket
@@ -613,16 +618,192 @@ __device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, i
     return ret;
 }
 
+// ---- fused deferred-MLP epilogue (KF_FUSED) ----------------------------------------------
+// When a warp's 32 rays have all ended, their accumulators are still in the lanes' registers:
+// the warp evaluates h(C_d, F, d) (Eq. 3; 34 -> 16 -> 16 -> 3) for its tile on
+// the tensor cores exactly as shade_mma_kernel does (split-fp16 operands, fp32 accumulation:
+// pixels are the M dimension, two m16 tiles), and stores the pixels.  The input rows are
+// transposed through ONE per-CTA staging buffer (16 rows x 2 halves planes, 3.5 KB) that the
+// CTA's warps take in turn (a shared-memory lock: tile ends are rare, ~1 per 0.1 ms per warp),
+// so the march keeps its L1 for the texel gathers.
+struct FusedSmem {
+    __half x[2][16][kXStride];     // [hi, lo][pixel row of the m16 tile][input]
+    float o[32][4];                // logits of the tile's pixels
+    int lock;
+};
+
+template <int KF>
+__device__ __noinline__ void fused_epilogue(const DevScene& S, const RaySource& rs, void* out, int64_t rbase,
+                                            const RayState st, FusedSmem& sm) {
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const int64_t r = rbase + lane;
+    bool valid = r < rs.n;
+    int view = 0, px = 0, py = 0;
+    float d[3] = {0.f, 0.f, 1.f};
+    if (valid) valid = ray_pixel(rs, rs.ray0 + r, view, px, py);
+    if (valid) {
+        const merf_camera& c = rs.cb.cam[view];
+        const float x0 = __fdividef((float)px + 0.5f - (float)c.cx, (float)c.fx);   // MLP input: fp32
+        const float x1 = __fdividef((float)py + 0.5f - (float)c.cy, (float)c.fy);
+        float v[3];
+#pragma unroll
+        for (int q = 0; q < 3; q++)
+            v[q] = fmaf((float)c.c2w[4 * q], x0, fmaf((float)c.c2w[4 * q + 1], x1, (float)c.c2w[4 * q + 2]));
+        const float inv = rsqrtf(fmaf(v[0], v[0], fmaf(v[1], v[1], v[2] * v[2])));
+#pragma unroll
+        for (int q = 0; q < 3; q++) d[q] = v[q] * inv;
+    }
+    if (lane == 0) {
+        while (atomicCAS(&sm.lock, 0, 1) != 0) __nanosleep(32);
+        __threadfence_block();
+    }
+    __syncwarp();
+    const uint4* tab = reinterpret_cast<const uint4*>(S.mlp_frag) + lane * (kMlpFragWords / 4);
+    const int lrow = (lane & 7) + ((lane >> 3) & 1) * 8, lcol = (lane >> 4) * 8;
+    float h3[2][4];
+#pragma unroll
+    for (int mt = 0; mt < 2; mt++) {
+        if ((lane >> 4) == mt) {
+            // this pixel's input row [C_d, F, d, sin/cos(2^k d_j) (j outer, k inner, D17), 0 pad]
+            // as 20 (hi, lo) half pairs: columns 0..39 (the k8 step reads 32..39)
+            uint32_t* ph = reinterpret_cast<uint32_t*>(&sm.x[0][lane & 15][0]);
+            uint32_t* pl = reinterpret_cast<uint32_t*>(&sm.x[1][lane & 15][0]);
+            uint32_t h, l;
+            split2(st.cd[0], st.cd[1], h, l); ph[0] = h; pl[0] = l;
+            split2(st.cd[2], st.F[0], h, l); ph[1] = h; pl[1] = l;
+            split2(st.F[1], st.F[2], h, l); ph[2] = h; pl[2] = l;
+            split2(st.F[3], d[0], h, l); ph[3] = h; pl[3] = l;
+            split2(d[1], d[2], h, l); ph[4] = h; pl[4] = l;
+            int w = 5;
+#pragma unroll
+            for (int j = 0; j < 3; j++) {
+                float sn = __sinf(d[j]), cs = __cosf(d[j]);
+#pragma unroll
+                for (int k = 0; k < 4; k++) {
+                    split2(sn, cs, h, l);
+                    ph[w] = h;
+                    pl[w] = l;
+                    w++;
+                    const float s2 = 2.f * sn * cs, c2 = fmaf(-2.f * sn, sn, 1.f);
+                    sn = s2;
+                    cs = c2;
+                }
+            }
+#pragma unroll
+            for (int q = 17; q < 20; q++) { ph[q] = 0u; pl[q] = 0u; }
+        }
+        __syncwarp();
+        // layer 1: [16 px x 34] x [34 x 16], bias in the accumulator
+        float c1[2][4];
+        {
+            const uint4 b01 = __ldg(tab + 8);                   // layer-1 biases (words 32..35)
+            c1[0][0] = c1[0][2] = __uint_as_float(b01.x);
+            c1[0][1] = c1[0][3] = __uint_as_float(b01.y);
+            c1[1][0] = c1[1][2] = __uint_as_float(b01.z);
+            c1[1][1] = c1[1][3] = __uint_as_float(b01.w);
+        }
+#pragma unroll
+        for (int s2 = 0; s2 < 2; s2++) {
+            uint32_t ah[4], al[4];
+            ldm4(ah, &sm.x[0][lrow][16 * s2 + lcol]);
+            ldm4(al, &sm.x[1][lrow][16 * s2 + lcol]);
+#pragma unroll
+            for (int nt = 0; nt < 2; nt++) {
+                const uint4 b = __ldg(tab + 2 * s2 + nt);
+                const uint32_t bb[4] = {b.x, b.y, b.z, b.w};
+                mma16x3(c1[nt], ah, al, bb);
+            }
+        }
+        {
+            uint32_t h0, h1, l0, l1;
+            ldm2(h0, h1, &sm.x[0][lrow][32]);
+            ldm2(l0, l1, &sm.x[1][lrow][32]);
+            const uint4 b = __ldg(tab + 4);                    // words 16..19
+            mma8(c1[0], l0, l1, b.x);
+            mma8(c1[0], h0, h1, b.y);
+            mma8(c1[0], h0, h1, b.x);
+            mma8(c1[1], l0, l1, b.z);
+            mma8(c1[1], h0, h1, b.w);
+            mma8(c1[1], h0, h1, b.z);
+        }
+        __syncwarp();                                          // staging rows free for the next m tile
+        // layer 2: ReLU(h1) [16 x 16] x [16 x 16]
+        uint32_t ah[4], al[4];
+        relu_to_a(c1[0], c1[1], ah, al);
+        float c2[2][4];
+        {
+            const uint4 b23 = __ldg(tab + 9);                   // layer-2 biases (words 36..39)
+            c2[0][0] = c2[0][2] = __uint_as_float(b23.x);
+            c2[0][1] = c2[0][3] = __uint_as_float(b23.y);
+            c2[1][0] = c2[1][2] = __uint_as_float(b23.z);
+            c2[1][1] = c2[1][3] = __uint_as_float(b23.w);
+        }
+#pragma unroll
+        for (int nt = 0; nt < 2; nt++) {
+            const uint4 b = __ldg(tab + 5 + nt);               // words 20..27
+            const uint32_t bb[4] = {b.x, b.y, b.z, b.w};
+            mma16x3(c2[nt], ah, al, bb);
+        }
+        // layer 3: ReLU(h2) [16 x 16] x [16 x 3 (padded to 8)]
+        relu_to_a(c2[0], c2[1], ah, al);
+        {
+            const uint4 b3 = __ldg(tab + 10);                  // words 40..43 (layer-3 biases)
+            h3[mt][0] = h3[mt][2] = __uint_as_float(b3.x);
+            h3[mt][1] = h3[mt][3] = __uint_as_float(b3.y);
+            const uint4 b = __ldg(tab + 7);                    // words 28..31
+            const uint32_t bb[4] = {b.x, b.y, b.z, b.w};
+            mma16x3(h3[mt], ah, al, bb);
+        }
+    }
+    if (t <= 1) {
+#pragma unroll
+        for (int mt = 0; mt < 2; mt++) {
+            *reinterpret_cast<float2*>(&sm.o[16 * mt + g][2 * t]) = make_float2(h3[mt][0], h3[mt][1]);
+            *reinterpret_cast<float2*>(&sm.o[16 * mt + g + 8][2 * t]) = make_float2(h3[mt][2], h3[mt][3]);
+        }
+    }
+    __syncwarp();
+    const float4 hv = *reinterpret_cast<const float4*>(&sm.o[lane][0]);
+    __syncwarp();
+    if (lane == 0) {
+        __threadfence_block();
+        atomicExch(&sm.lock, 0);
+    }
+    if (!valid) return;
+    const float c0 = __saturatef(st.cd[0] + __fdividef(1.0f, 1.0f + __expf(-hv.x)));
+    const float c1 = __saturatef(st.cd[1] + __fdividef(1.0f, 1.0f + __expf(-hv.y)));
+    const float c2 = __saturatef(st.cd[2] + __fdividef(1.0f, 1.0f + __expf(-hv.z)));
+    const int64_t idx = out_index(rs, view, px, py);
+    if (KF & KF_U8) {
+        reinterpret_cast<uchar4*>(out)[idx] =
+            make_uchar4((unsigned char)__float2int_rn(c0 * 255.f), (unsigned char)__float2int_rn(c1 * 255.f),
+                        (unsigned char)__float2int_rn(c2 * 255.f), 255);
+    } else {
+        float* o3 = reinterpret_cast<float*>(out) + 3 * idx;
+        o3[0] = c0;
+        o3[1] = c1;
+        o3[2] = c2;
+    }
+}
+
 // Persistent march.  Every lane owns one ray at a time; a warp takes the next tile of 32
 // coherent rays from the global queue once all its lanes are idle (refilling single lanes or
 // half tiles breaks the coherence the skipping relies on: measured 1.5-2x and 1.27x slower).
 // Each round is one traversal step of every lane holding a ray (segment transition, probe,
 // skip or find) followed by the shading of the lanes that found a sample.
 template <int KF>
-__global__ void __launch_bounds__(kMarchThreads, MERF_MARCH_MINB) march_kernel(DevScene S, int64_t n_rays, Workspace ws,
+__global__ void __launch_bounds__(kMarchThreads, MERF_MARCH_MINB) march_kernel(const __grid_constant__ DevScene S,
+                                                              int64_t n_rays, Workspace ws,
                                                               uint32_t rflags, TraceArgs ta,
-                                                              unsigned long long* stats, MarchTune tune) {
+                                                              unsigned long long* stats, MarchTune tune,
+                                                              const __grid_constant__ RaySource rs, void* out) {
     const unsigned FULL = 0xffffffffu;
+    __shared__ __align__(16) FusedSmem fsm[(KF & KF_FUSED) ? 1 : 1];
+    if (KF & KF_FUSED) {
+        if (threadIdx.x == 0) fsm[0].lock = 0;
+        __syncthreads();
+    }
+    int64_t tile_rbase = -1;           // chunk-local first ray of the warp's current tile (fused epilogue)
     const int lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
     const int nl = S.n_levels;
@@ -650,7 +831,7 @@ __global__ void __launch_bounds__(kMarchThreads, MERF_MARCH_MINB) march_kernel(D
     }
 
     auto finish = [&]() {
-        store_accum(ws.accum + (int64_t)ray * 2, st);
+        if (!(KF & KF_FUSED)) store_accum(ws.accum + (int64_t)ray * 2, st);
         if (KF & KF_TRACE) ta.counts[ray] = n_eval;
         ray = -1;
     };
@@ -659,6 +840,7 @@ __global__ void __launch_bounds__(kMarchThreads, MERF_MARCH_MINB) march_kernel(D
         // ---------------- tile scheduling: a new tile of 32 rays when the warp is empty -------
         unsigned act = __ballot_sync(FULL, ray >= 0);
         if (act == 0) {
+            if ((KF & KF_FUSED) && tile_rbase >= 0) fused_epilogue<KF>(S, rs, out, tile_rbase, st, fsm[0]);
             int tile = 0;
             if (lane == 0) {
                 int t = (int)atomicAdd(ws.queue, 1u);
@@ -674,6 +856,7 @@ __global__ void __launch_bounds__(kMarchThreads, MERF_MARCH_MINB) march_kernel(D
             }
             tile = __shfl_sync(FULL, tile, 0);
             const unsigned base = (unsigned)tile << 5;
+            tile_rbase = base;
             if (tile >= ws.n_tiles) {
                 if ((KF & KF_COUNT) && lane == 0) atomicMin(stats + 17, gtime());
                 break;
@@ -689,7 +872,7 @@ __global__ void __launch_bounds__(kMarchThreads, MERF_MARCH_MINB) march_kernel(D
                 st.cd[0] = st.cd[1] = st.cd[2] = 0.f;
                 st.F[0] = st.F[1] = st.F[2] = st.F[3] = 0.f;
                 if (ns > 0) {
-                    const int4* p = ws.seg + ((int64_t)ray * kMaxSeg) * 2;
+                    const int4* p = ws.seg + ((int64_t)ray * ws.seg_slots) * 2;
                     qa = p[0];
                     uu = p[1];
                 } else {
@@ -742,7 +925,7 @@ __global__ void __launch_bounds__(kMarchThreads, MERF_MARCH_MINB) march_kernel(D
             if (k >= qa.w) {                                  // segment exhausted
                 j++;
                 if (j >= ns) { finish(); return; }
-                const int4* p = ws.seg + ((int64_t)ray * kMaxSeg + j) * 2;
+                const int4* p = ws.seg + ((int64_t)ray * ws.seg_slots + j) * 2;
                 qa = p[0];
                 uu = p[1];
                 k = 0;

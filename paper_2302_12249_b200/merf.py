@@ -113,7 +113,8 @@ SIGNATURES = [
     ("merf_scene_load", C.c_int, [C.c_char_p, _i32, C.POINTER(_vp)]),
     ("merf_cameras_read", C.c_int, [C.c_char_p, C.POINTER(merf_camera), _i32, C.POINTER(_i32), _vp, _vp]),
     ("merf_build_block_index", C.c_int, [_vp, C.POINTER(merf_scene_desc), _vp, C.POINTER(_i64), _vp]),
-    ("merf_render_workspace_bytes", C.c_int, [_vp, _i32, _i32, _i32, C.POINTER(_i64), C.POINTER(_i64)]),
+    ("merf_render_workspace_bytes", C.c_int, [_vp, C.POINTER(merf_camera), _i32, _i32, _i32, C.POINTER(_i64),
+                                              C.POINTER(_i64)]),
     ("merf_render_shard_blocks", C.c_int, [_vp, C.POINTER(merf_camera), _i32, _i32, _i32, _i32, _i32, _i32, _vp,
                                            _u32, _vp]),
     ("merf_shard_slots", _i32, [_i32, _i32, _i32]),
@@ -277,10 +278,11 @@ def merf_render_shard(handle, cams, W: int, H: int, part_rank: int, part_count: 
                                    int(fmt), _ptr(out), int(flags), _stream(stream)))
 
 
-def merf_render_workspace_bytes(handle, n_cams: int, W: int, H: int) -> dict:
-    """device workspace of a merf_render call: bytes per chunk and rays per chunk."""
+def merf_render_workspace_bytes(handle, cams, W: int, H: int) -> dict:
+    """device workspace of a merf_render(cams, W, H) call: bytes per chunk and rays per chunk."""
     b, r = C.c_int64(), C.c_int64()
-    _check(lib().merf_render_workspace_bytes(handle, int(n_cams), int(W), int(H), C.byref(b), C.byref(r)))
+    carr = cameras_to_c(cams)
+    _check(lib().merf_render_workspace_bytes(handle, carr, len(carr), int(W), int(H), C.byref(b), C.byref(r)))
     return {"bytes": b.value, "rays_per_chunk": r.value, "bytes_per_ray": b.value / max(r.value, 1)}
 
 

@@ -129,6 +129,8 @@ def test_ptxas_has_no_spills(M):
                 assert v["spill_st"] <= 128, (k, v)
             elif kf & 512:  # KF_SPH: the NEXT-2 comparison variant (fp32 curve state), not production
                 assert v["spill_st"] <= 16 and v["regs"] <= 56, (k, v)
+            elif kf & 1024:  # KF_FUSED: the fused-MLP experiment (measured slower, opt-in): spills
+                assert v["spill_st"] <= 256 and v["regs"] <= 56, (k, v)   # in its noinline epilogue
             else:           # production variants: registers only, at the 9-CTA/SM cap
                 assert v["spill_st"] == 0 and v["stack"] == 0 and v["regs"] <= 56, (k, v)
         elif k == "setup_kernel<0>":
