@@ -8,16 +8,6 @@ namespace merf {
 
 constexpr int kMaxDevices = 64;
 
-static MarchTune march_tune() {
-    static MarchTune t = [] {
-        MarchTune d{kShadeMin, kTravSteps};
-        if (const char* e = getenv("MERF_TUNE")) sscanf(e, "%d,%d", &d.shade_min, &d.trav_steps);
-        if (d.trav_steps < 1) d.trav_steps = 1;
-        return d;
-    }();
-    return t;
-}
-
 template <int KF>
 static cudaError_t march_v(const DevScene& S, int64_t n, const Workspace& ws, uint32_t rflags,
                            const TraceArgs& ta, unsigned long long* stats, cudaStream_t st,
@@ -40,7 +30,7 @@ static cudaError_t march_v(const DevScene& S, int64_t n, const Workspace& ws, ui
     int grid = (int)(need < blocks ? need : blocks);
     cudaError_t e = cudaMemsetAsync(ws.queue, 0, sizeof(unsigned int), st);
     if (e != cudaSuccess) return e;
-    march_kernel<KF><<<grid, kMarchThreads, 0, st>>>(S, n, ws, rflags, ta, stats, march_tune(), rs, out);
+    march_kernel<KF><<<grid, kMarchThreads, 0, st>>>(S, n, ws, rflags, ta, stats, rs, out);
     return cudaGetLastError();
 }
 

@@ -66,16 +66,12 @@ constexpr int kSetupThreads = 128;
 #define MERF_MARCH_MINB 9
 #endif
 constexpr int kMarchThreads = MERF_MARCH_THREADS;
-// March scheduling policy, tuned on B200 (bench workload sweeps): a warp takes a new tile of
-// 32 rays only when all its lanes are idle (per-lane refill broke the tile coherence the
+// March scheduling policy, tuned on B200 (bench workload sweeps, r01): a warp takes a new tile
+// of 32 rays only when all its lanes are idle (per-lane refill broke the tile coherence the
 // skipping relies on and was 1.5-2x slower).  A round = one traversal step of every lane
 // holding a ray, then the shading of the lanes that found a sample; further warp-synchronous
-// steps (until kShadeMin lanes are ready, at most kTravSteps) measured slower than going
-// straight to shading once the per-step ballot cost dropped: (16, 16) 1315, (8, 16) 1324,
-// (1, 16) 1337, (1, 1) 1369 M rays/s.  MERF_TUNE="shade_min,trav_steps" overrides.
-constexpr int kShadeMin = 1;
-constexpr int kTravSteps = 1;
-struct MarchTune { int shade_min, trav_steps; };   // runtime override (MERF_TUNE="shade,steps")
+// steps (until k lanes are ready, at most m steps) measured slower once the per-step ballot
+// cost dropped: (16, 16) 1315, (8, 16) 1324, (1, 16) 1337, (1, 1) 1369 M rays/s.
 
 // ------------------------------------------------------------------------------------
 // ray indexing: camera rays are numbered in 8x4-pixel tile order (32 rays per tile, one
@@ -795,7 +791,7 @@ template <int KF>
 __global__ void __launch_bounds__(kMarchThreads, MERF_MARCH_MINB) march_kernel(const __grid_constant__ DevScene S,
                                                               int64_t n_rays, Workspace ws,
                                                               uint32_t rflags, TraceArgs ta,
-                                                              unsigned long long* stats, MarchTune tune,
+                                                              unsigned long long* stats,
                                                               const __grid_constant__ RaySource rs, void* out) {
     const unsigned FULL = 0xffffffffu;
     __shared__ __align__(16) FusedSmem fsm[(KF & KF_FUSED) ? 1 : 1];
@@ -883,11 +879,10 @@ __global__ void __launch_bounds__(kMarchThreads, MERF_MARCH_MINB) march_kernel(c
         }
 
         // ---------------- traversal: advance lanes towards their next evaluated sample ----
-        // One step per lane per round by default (MarchTune: further warp-synchronous steps
-        // while fewer than shade_min lanes are ready); lanes in long empty stretches keep
-        // skipping in the next rounds, so one lane's skip chain never idles the warp.
+        // One step per lane per round; lanes in long empty stretches keep skipping in the next
+        // rounds, so one lane's skip chain never idles the warp.
         bool found = false;
-        int Qx = 0, Qy = 0, Qz = 0, fcell = 0;
+        int Qx, Qy, Qz, fcell;             // set by the step that finds a sample (read only then)
         // one traversal step of a lane that wants a sample
         auto step = [&]() {
             if (KF & KF_SPH) {
@@ -1007,18 +1002,10 @@ __global__ void __launch_bounds__(kMarchThreads, MERF_MARCH_MINB) march_kernel(c
                 found = true;
             }
         };
-        // the first step runs for every lane holding a ray (none has found a sample yet);
-        // further steps only while lanes still search and fewer than shade_min are ready
+        // one step for every lane holding a ray, then the shading (a round; §6 Rounds: further
+        // warp-synchronous steps before shading measured slower, so the r01 tuning knob is gone)
         if (KF & KF_COUNT) c_steps += lane == 0;
         if (ray >= 0) step();
-        for (int it = 1; it < tune.trav_steps; it++) {
-            const bool want = ray >= 0 && !found;
-            const unsigned m_want = __ballot_sync(FULL, want);
-            if (m_want == 0) break;
-            if (KF & KF_COUNT) c_steps += lane == 0;
-            if (__popc(act & ~m_want) >= tune.shade_min) break;   // lanes ready to shade
-            if (want) step();
-        }
 
         // ---------------- shading (converged) ----------------
         if (KF & KF_COUNT) {
