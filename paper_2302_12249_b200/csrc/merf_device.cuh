@@ -282,13 +282,18 @@ constexpr uint32_t kMagicBits = 0x4B400000u;   // its bit pattern (low 22 bits z
 __device__ __forceinline__ int exit_axis(int Qa, int U, int lo, int hi, int K) {
     const int a = abs(U);
     const int num = U > 0 ? hi - Qa : Qa - lo + 1;
-    // ceil of the estimate num * rcp(a) in one FFMA rounding up onto the integer grid of the
-    // 1.5 * 2^23 magic (exact below 2^22; positive float bit patterns are monotonic, so any larger,
-    // infinite or NaN quotient (a = 0) still clamps to K): no FRND / F2I on the XU pipe
-    const float t = __fmaf_ru((float)num, rcp_ftz((float)a), kMagicF);
+    // ceil of the estimate num * rcp(a) (1 - 2^-22) in one FFMA rounding up onto the integer grid
+    // of the 1.5 * 2^23 magic (exact below 2^22; positive float bit patterns are monotonic, so
+    // any larger, infinite or NaN quotient (a = 0) still clamps to K): no FRND / F2I on the XU
+    // pipe.  MUFU rcp is within 2^-23 of 1/a and (float)num within 2^-24 of num, so the biased
+    // product is never above num / a and, for num / a < 2^21, above num / a - 1: the estimate is
+    // ceil(num / a) or one less, and one upward correction makes it exact.  (Beyond 2^21 -- a
+    // skip of > 2M samples, only at steps below 2^-18 -- it may land short of the exit, inside
+    // the same empty cell, which the next probe skips again: never past an occupied sample.)
+    const float rc = rcp_ftz((float)a) * 0.99999976158142090f;       // 1 - 2^-22
+    const float t = __fmaf_ru((float)num, rc, kMagicF);
     int e = min((int)(__float_as_uint(t) - kMagicBits), K);
     e += (e * a < num) ? 1 : 0;
-    e -= ((e - 1) * a >= num) ? 1 : 0;
     return min(e, K);
 }
 
