@@ -512,15 +512,12 @@ __device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, i
 #pragma unroll
         for (int c = 0; c < 4; c++) wV[c] = wleaf(yi[c], yf[c], vf[0]);
         if (ALL) {
-            // branch-free: a missing block (impossible in a scene that passed the upload's
-            // soundness check, but defined: it contributes nothing) reads block 0 with zero
-            // weights, so neither pass needs a divergent region around the V gather
-            if (blk < 0) {
-                n_src -= 1;
-                ret = 2;
-#pragma unroll
-                for (int c = 0; c < 4; c++) wV[c] = 0u;
-            }
+            // An evaluated sample lies in an occupied finest cell, and the upload rejects any
+            // scene in which such a cell's trilinear base voxel has no block (block_need +
+            // block_check, MERF_EMISMATCH): the block exists.  The clamp only keeps a corrupted
+            // index in bounds (MERF_BOUNDS_CHECK builds trap on it instead); the r01 branch-free
+            // zero-weight handling of a missing block cost 7 issued instructions per sample.
+            MERF_CHECK(blk >= 0);
             blk = max(blk, 0);
         }
         if (ALL || blk >= 0) {
