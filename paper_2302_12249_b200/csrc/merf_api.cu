@@ -160,6 +160,10 @@ static void fill_dev(merf_scene* s) {
         S.log2_step = (float)std::log2(d.step);
         S.ka_l2n = (float)(-2.0 * d.m_appearance / 255.0 / 65535.0 * l2e);
         S.ma_l2 = (float)(d.m_appearance * l2e);
+        // the device's fp32 fmaf / product with n = 4, evaluated exactly as the kernel would
+        // (fma rounds once: std::fma on floats), so the folded constants change no bit
+        S.dens_off4 = std::fma(4.0f, -S.md_l2, S.log2_step);
+        S.ma_l2_4 = 4.0f * S.ma_l2;
     }
     S.use_v = S.L > 0;
     for (int a = 0; a < 3; a++) S.use_p[a] = S.R > 0 && ((d.source_mask >> (1 + a)) & 1u);

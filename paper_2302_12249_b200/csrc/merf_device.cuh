@@ -63,6 +63,7 @@ struct DevScene {
     float kd_l2, md_l2, log2_step;   // base-2 forms: log2(tau Delta) = s kd_l2 - n md_l2 + log2_step
     float kd_l2w;                 // kd_l2 / 65535 (density sum in 16-bit weight units)
     float ka_l2n, ma_l2;          // sigmoid argument: -x log2e = acc ka_l2n + n ma_l2
+    float dens_off4, ma_l2_4;     // the n = 4 constants: fmaf(4, -md_l2, log2_step), 4 ma_l2
     int n_src;                    // active sources (V counted only when L > 0)
     int use_v, use_p[3];
     double step;                  // Delta (power of two)

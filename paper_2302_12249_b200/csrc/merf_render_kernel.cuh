@@ -570,7 +570,10 @@ __device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, i
     }
     // tau = exp(t0), t0 = s0 kd - n m (Eq. 6-7), s0 = sd / 65535; alpha = 1 - exp(-tau Delta)
     // in base 2: log2(tau Delta) = sd kd log2e / 65535 - n m log2e + log2 Delta (one FFMA)
-    const float tau_step = ex2_ftz(fmaf((float)(int)sd, S.kd_l2w, fmaf((float)n_src, -S.md_l2, S.log2_step)));
+    // (all-sources instance: the constant term -4 m log2e + log2 Delta precomputed at upload,
+    // bit-identical to the fmaf below with n_src = 4)
+    const float tau_step = ex2_ftz(fmaf((float)(int)sd, S.kd_l2w,
+                                        ALL ? S.dens_off4 : fmaf((float)n_src, -S.md_l2, S.log2_step)));
     const float alpha = 1.f - ex2_ftz(tau_step * -1.4426950408889634f);
     if (alpha > S.alpha_skip) {
         // ---- appearance pass: 20 AoS texels, channels 1..7, the same weights + dp2a
@@ -596,7 +599,7 @@ __device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, i
             for (int dv = 0; dv < 2; dv++) acc_pair(acc, __ldg(row + dv * R), wP[a][dv]);
         }
         // sigmoid(x), x = acc ka / 65535 - n m: 1 / (1 + 2^(-x log2e)), the exponent in one FFMA
-        const float off = (float)n_src * S.ma_l2;
+        const float off = ALL ? S.ma_l2_4 : (float)n_src * S.ma_l2;
         const float w = alpha * st.T;
 #pragma unroll
         for (int c = 0; c < 3; c++)
