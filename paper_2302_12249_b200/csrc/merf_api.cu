@@ -284,14 +284,13 @@ extern "C" merf_status merf_scene_upload(const merf_scene_desc* desc, const uint
         UPC_TRY(cudaMallocAsync((void**)&d_pl, pb, cs));
         UPC_TRY(cudaMemcpyAsync(d_pl, planes, pb, cudaMemcpyHostToDevice, cs));
         uint4* d_pp;
-        // padded by one entry row: the clamped upper-edge row (weight 0) stays in bounds
-        const size_t ppb = ((size_t)3 * desc->R * desc->R + desc->R) * 16;
+        // [3][R + 1][R]: row R of each plane repeats row R - 1 (the upper-edge corner, texel())
+        const size_t ppb = (size_t)3 * (desc->R + 1) * desc->R * 16;
         UP_TRY(dalloc(s, &d_pp, ppb));
-        UPC_TRY(cudaMemsetAsync(d_pp, 0, ppb, cs));
         UPC_TRY(launch_pack_pairs(d_pl, desc->R, d_pp, nullptr, 0, nullptr, cs));
         S.plane_pairs = d_pp;
         uint32_t* d_pd;
-        UP_TRY(dalloc(s, &d_pd, (size_t)3 * desc->R * desc->R * 4));
+        UP_TRY(dalloc(s, &d_pd, (size_t)3 * (desc->R + 1) * desc->R * 4));
         UPC_TRY(launch_pack_density(d_pl, desc->R, d_pd, nullptr, 0, nullptr, cs));
         S.pdens = d_pd;
         UPC_TRY(cudaFreeAsync(d_pl, cs));
@@ -363,6 +362,8 @@ extern "C" merf_status merf_scene_upload(const merf_scene_desc* desc, const uint
             UPC_TRY(cudaMemcpyAsync(d_at, atlas, ab, cudaMemcpyHostToDevice, cs));
         }
         S.block_index = d_idx;
+        // outside-the-grid aprons of edge blocks repeat the edge voxels (texel(), D9)
+        if (d_at) UPC_TRY(launch_apron_edge(d_idx, desc->L, n_blocks, d_at, cs));
         uint4* d_ap;
         UP_TRY(dalloc(s, &d_ap, (size_t)n_blocks * 648 * 16));
         if (n_blocks) UPC_TRY(launch_pack_pairs(nullptr, 0, nullptr, d_at, n_blocks, d_ap, cs));

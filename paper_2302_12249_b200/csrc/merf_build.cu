@@ -161,13 +161,14 @@ __global__ void contract_kernel(const double* __restrict__ x, int64_t n, double*
 // the density bytes of its bilinear quad (u..u+1, v..v+1); a grid base voxel holds the
 // density bytes of its trilinear octet from the block's 9^3 apron storage.  One load then
 // fetches all corners of a source for the density pass (P:311 texture split).
+// density quads in the [3][R + 1][R] layout (row R of each plane repeats row R - 1)
 __global__ void pack_plane_density_kernel(const uint8_t* __restrict__ planes, int R,
                                           uint32_t* __restrict__ pdens) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    int64_t n = (int64_t)3 * R * R;
+    int64_t n = (int64_t)3 * (R + 1) * R;
     if (i >= n) return;
-    int a = (int)(i / ((int64_t)R * R));
-    int v = (int)((i / R) % R), u = (int)(i % R);
+    int a = (int)(i / ((int64_t)(R + 1) * R));
+    int v = min((int)((i / R) % (R + 1)), R - 1), u = (int)(i % R);
     int u1 = min(u + 1, R - 1), v1 = min(v + 1, R - 1);
     const uint8_t* pl = planes + (size_t)a * R * R * 8;
     uint32_t q = (uint32_t)pl[((size_t)v * R + u) * 8] | ((uint32_t)pl[((size_t)v * R + u1) * 8] << 8) |
@@ -308,7 +309,7 @@ cudaError_t launch_block_check(const uint8_t* need, const int32_t* index, int64_
 cudaError_t launch_pack_density(const uint8_t* planes, int R, uint32_t* pdens, const uint8_t* atlas,
                                 int64_t n_blocks, uint2* vdens, cudaStream_t st) {
     if (planes && R > 0)
-        pack_plane_density_kernel<<<blocks_for((int64_t)3 * R * R, 256), 256, 0, st>>>(planes, R, pdens);
+        pack_plane_density_kernel<<<blocks_for((int64_t)3 * (R + 1) * R, 256), 256, 0, st>>>(planes, R, pdens);
     if (atlas && n_blocks > 0)
         pack_voxel_density_kernel<<<blocks_for(n_blocks * 512, 256), 256, 0, st>>>(atlas, n_blocks, vdens);
     return cudaGetLastError();
@@ -432,12 +433,15 @@ __device__ __forceinline__ uint4 pair_entry(uint2 a, uint2 b) {
 }
 
 __global__ void pack_plane_pairs_kernel(const uint2* __restrict__ planes, int R, uint4* __restrict__ out) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // entry (a, v, u)
-    const int64_t n = (int64_t)3 * R * R;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // entry (a, v, u), v <= R
+    const int64_t n = (int64_t)3 * (R + 1) * R;
     if (i >= n) return;
     const int u = (int)(i % R);
-    const uint2 a = planes[i];
-    const uint2 b = u + 1 < R ? planes[i + 1] : a;    // u + 1 = R: weight 0 (clamped texel)
+    const int a_ = (int)(i / ((int64_t)(R + 1) * R));
+    const int v = min((int)((i / R) % (R + 1)), R - 1);                  // row R repeats row R - 1
+    const int64_t src = ((int64_t)a_ * R + v) * R + u;
+    const uint2 a = planes[src];
+    const uint2 b = u + 1 < R ? planes[src + 1] : a;  // u + 1 = R repeats texel R - 1 (edge)
     out[i] = pair_entry(a, b);
 }
 
@@ -450,10 +454,40 @@ __global__ void pack_atlas_pairs_kernel(const uint2* __restrict__ atlas, int64_t
     out[i] = pair_entry(src[0], src[1]);
 }
 
+// The + side apron (local index 8) of a block on the grid's upper edge lies outside the grid;
+// the renderer's texel() reads it as the corner past texel L-1, which must repeat texel L-1
+// (clamp to edge, D9).  Rewrite those apron voxels of the staging atlas (our device copy of the
+// caller's AoS atlas) from the edge voxels before the packed layouts are built.
+__global__ void apron_edge_kernel(const int32_t* __restrict__ index, int64_t slots, int nb, int64_t n_blocks,
+                                  uint2* __restrict__ atlas) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // (slot, voxel of 9^3)
+    if (i >= slots * 729) return;
+    const int64_t slot = i / 729;
+    const int l = (int)(i - slot * 729);
+    const int bx = (int)(slot % nb), by = (int)((slot / nb) % nb), bz = (int)(slot / ((int64_t)nb * nb));
+    if (bx != nb - 1 && by != nb - 1 && bz != nb - 1) return;
+    const int32_t b = index[slot];
+    if (b < 0 || b >= n_blocks) return;
+    const int lx = l % 9, ly = (l / 9) % 9, lz = l / 81;
+    const int sx = (bx == nb - 1) ? min(lx, 7) : lx, sy = (by == nb - 1) ? min(ly, 7) : ly,
+              sz = (bz == nb - 1) ? min(lz, 7) : lz;
+    if (sx == lx && sy == ly && sz == lz) return;                    // not an outside-the-grid apron voxel
+    atlas[(size_t)b * 729 + l] = atlas[(size_t)b * 729 + (sz * 9 + sy) * 9 + sx];
+}
+
+cudaError_t launch_apron_edge(const int32_t* index, int L, int64_t n_blocks, uint8_t* atlas, cudaStream_t st) {
+    const int nb = L / 8;
+    const int64_t slots = (int64_t)nb * nb * nb;
+    if (n_blocks <= 0) return cudaSuccess;
+    apron_edge_kernel<<<(unsigned)((slots * 729 + 255) / 256), 256, 0, st>>>(index, slots, nb, n_blocks,
+                                                                          reinterpret_cast<uint2*>(atlas));
+    return cudaGetLastError();
+}
+
 cudaError_t launch_pack_pairs(const uint8_t* planes, int R, uint4* plane_pairs, const uint8_t* atlas,
                               int64_t n_blocks, uint4* atlas_pairs, cudaStream_t st) {
     if (planes && R > 0) {
-        const int64_t n = (int64_t)3 * R * R;
+        const int64_t n = (int64_t)3 * (R + 1) * R;
         pack_plane_pairs_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
             reinterpret_cast<const uint2*>(planes), R, plane_pairs);
     }

@@ -37,10 +37,10 @@ struct DevScene {
     // appearance layouts, pair-interleaved along the fastest axis: entry (.., u) holds texels u
     // and u+1 as 4 words (c1 c1' c2 c2' | c3 c3' c4 c4' | c5 c5' c6 c6' | c7 c7' c0 c0'), so
     // one 16-byte load feeds 7 dp2a directly (no byte gathering)
-    const uint4* plane_pairs;     // [3][R][R] (+ one padding row)
+    const uint4* plane_pairs;     // [3][R + 1][R]: row R of each plane repeats row R - 1
     const int32_t* block_index;   // [(L/8)^3]
     const uint4* atlas_pairs;     // [n_blocks][9][9][8]
-    const uint32_t* pdens;        // [3][R][R] density quads, byte du + 2 dv
+    const uint32_t* pdens;        // [3][R + 1][R] density quads, byte du + 2 dv (same rows)
     const uint2* vdens;           // [n_blocks][8][8][8] density octets, byte dx + 2 dy + 4 dz
     const uint32_t* occ[MERF_MAX_LEVELS];
     const uint32_t* occ_fin;      // = occ[n_levels - 1] (static offset: no dynamic param indexing)
@@ -299,12 +299,16 @@ __device__ __forceinline__ int exit_axis(int Qa, int U, int lo, int hi, int K) {
 }
 
 // texel coordinate on a grid of resolution M = 2^m (s = F + 2 - m): lower index, fraction
-// (cell-centred texels, clamp to edge; reading D9).  Clamping the position to
-// [texel 0, texel M-1] gives the same interpolated value as the (M-2, f = 1) convention at
-// the upper edge: the extra corner i0 + 1 = M carries weight 0 (the layouts are padded so
-// that it is a valid address).
+// (cell-centred texels, clamp to edge; reading D9).  The position is clamped at texel 0 only:
+// past the centre of texel M-1 (the last half texel of the contracted cube, and lattice drift)
+// i0 = M-1 with 0 < f <= 1/2 + drift, and corner i0 + 1 = M is stored as a copy of texel M-1
+// in every layout (the planes' extra row per plane and pair entry (M-1, M-1), the atlas apron
+// of edge blocks, made to replicate the edge at upload).  The integer weights of the two
+// corners sum to their parent exactly, so this is bit-identical to clamping the position to
+// texel M-1 (f = 0), without the min on every axis of every sample.
 __device__ __forceinline__ void texel(int Qb, int s, int M, int& i0, float& f) {
-    const int P = min(max(Qb - (1 << (s - 1)), 0), (M - 1) << s);
+    (void)M;
+    const int P = max(Qb - (1 << (s - 1)), 0);
     i0 = P >> s;
     f = (float)(P & ((1 << s) - 1)) * __int_as_float((127 - s) << 23);
 }
@@ -322,7 +326,8 @@ __device__ __forceinline__ void texel(int Qb, int s, int M, int& i0, float& f) {
 
 __device__ __forceinline__ float exp2i(int n) { return __int_as_float((127 + n) << 23); }
 __device__ __forceinline__ void texel_g(int Qb, int s, int M, int& i0, float& g) {
-    const int P = min(max(Qb - (1 << (s - 1)), 0), (M - 1) << s);
+    (void)M;
+    const int P = max(Qb - (1 << (s - 1)), 0);        // upper edge: see texel()
     i0 = P >> s;
     unsigned b;                        // (P & mask) | 0x4B000000 in one LOP3
     asm("lop3.b32 %0, %1, %2, %3, 0xea;" : "=r"(b) : "r"(P), "r"((1 << s) - 1), "r"(0x4B000000));

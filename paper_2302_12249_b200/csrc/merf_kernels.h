@@ -66,5 +66,6 @@ cudaError_t launch_qat(const DevScene& S, const RaySource& rs, const Workspace& 
                        unsigned long long* n_samples, int L, int R, int Nf, const uint32_t* occf, float md, float ma,
                        cudaStream_t st);
 cudaError_t launch_stats_fold(unsigned long long* stats, cudaStream_t st);
+cudaError_t launch_apron_edge(const int32_t* index, int L, int64_t n_blocks, uint8_t* atlas, cudaStream_t st);
 
 }  // namespace merf

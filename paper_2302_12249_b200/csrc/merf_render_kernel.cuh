@@ -248,7 +248,7 @@ __device__ __forceinline__ float probe_od(const DevScene& S, int Qx, int Qy, int
 #pragma unroll
         for (int a = 0; a < 3; a++)
             if (S.use_p[a]) {
-                sum += __ldg(S.pdens + ((unsigned)(a * R + v[a]) * R + u[a])) & 0xFFu;
+                sum += __ldg(S.pdens + ((unsigned)(a * (R + 1) + v[a]) * R + u[a])) & 0xFFu;
                 n++;
             }
     }
@@ -433,19 +433,21 @@ __device__ __forceinline__ void store_accum(float4* a, const RayState& st) {
 }
 
 
-// Linear index of texel (v, u) of plane a in the [3][R][R] layouts.  With the paper geometry
-// the fields are disjoint bit ranges, so one 32-bit OR chain (the plane offset never becomes
-// a separate 64-bit pointer add).
+// Linear index of texel (v, u) of plane a in the [3][R + 1][R] layouts (row R of each plane
+// repeats row R - 1: the upper-edge corner of texel(), see merf_device.cuh).  With the paper
+// geometry a (R + 1) R = a (2^22 + 2^11) is a constant, so one 32-bit three-input add (the
+// plane offset never becomes a separate 64-bit pointer add).
 template <int KF>
 __device__ __forceinline__ unsigned plane_index(int a, int R, int v, int u) {
     if (KF & KF_PAPER) {
         // opaque to the compiler: it would otherwise peel the plane offset off into a 64-bit
         // pointer add (IADD3 + IMAD.X per access) after the 32-bit index scaling
         unsigned idx;
-        asm("lop3.b32 %0, %1, %2, %3, 0xfe;" : "=r"(idx) : "r"((unsigned)a << 22), "r"((unsigned)v << 11), "r"((unsigned)u));
+        asm("add.u32 %0, %1, %2;" : "=r"(idx) : "r"((unsigned)a * (unsigned)((kPaperR + 1) * kPaperR) + ((unsigned)v << 11)),
+            "r"((unsigned)u));
         return idx;
     }
-    return (unsigned)((a * R + v) * R + u);
+    return (unsigned)((a * (R + 1) + v) * R + u);
 }
 
 // Appearance accumulation of a corner PAIR from its pair-interleaved 16-byte entry (see
