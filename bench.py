@@ -60,7 +60,8 @@ def make_comm(M, rank: int, world: int, device: int):
     store (plumbing only)."""
     import torch.distributed as dist
     uid = [M.merf_comm_unique_id() if rank == 0 else None]
-    dist.broadcast_object_list(uid, src=0)
+    if world > 1:
+        dist.broadcast_object_list(uid, src=0)
     return M.Comm(uid[0], world, rank, device)
 
 
@@ -256,7 +257,8 @@ def e2e_multi(M, scene, comm, batches, args, rank, world, dev, stream, gstream, 
     for i, s in enumerate(range(min(2, args.warmup))):
         one(s, i)
     torch.cuda.synchronize()
-    dist.barrier()
+    if world > 1:
+        dist.barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -268,7 +270,8 @@ def e2e_multi(M, scene, comm, batches, args, rank, world, dev, stream, gstream, 
     comm.wait(stream=stream, timeout_ms=120000)
     torch.cuda.synchronize()
     t = torch.tensor([e0.elapsed_time(e1)], device=dev)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ems = float(t.item())
     return {"value": total_rays / (ems / 1e3), "unit": "rays/s",
             "h2d_bytes_per_step": world * V * 136, "d2h_bytes_per_step": world * V * W_IMG * H_IMG * 4,
@@ -286,6 +289,9 @@ def main():
     ap.add_argument("--views", type=int, default=16, help="views per rank per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--force-gather", action="store_true",
+                    help="run the N > 1 frame-gather and e2e path through a 1-rank NCCL communicator "
+                         "(exercises it on one GPU; not a scaling measurement)")
     ap.add_argument("--spherical", action="store_true",
                     help="NEXT-2 comparison: the scene baked in the spherical contraction's space, "
                          "rendered with fixed contracted-arc-length steps and no AABB skipping")
@@ -330,10 +336,13 @@ def main():
     stream = torch.cuda.Stream()
     gstream = torch.cuda.Stream()
     frames = [torch.empty((V, H_IMG, W_IMG, 4), dtype=torch.uint8, device=dev) for _ in range(2)]
-    comm = make_comm(M, rank, world, local) if world > 1 else None
+    # the frame gather runs at N > 1 (and, to exercise the N > 1 code path on one GPU, with a
+    # 1-rank communicator under --force-gather)
+    gathering = world > 1 or args.force_gather
+    comm = make_comm(M, rank, world, local) if gathering else None
     # the root's gather targets: [world][V][H][W][4], double buffered like the frames
     root_bufs = ([torch.empty((world, V, H_IMG, W_IMG, 4), dtype=torch.uint8, device=dev) for _ in range(2)]
-                 if world > 1 and rank == 0 else [None, None])
+                 if gathering and rank == 0 else [None, None])
 
     # ---- counters pass over exactly the launches timed below (untimed, same views)
     algo_bytes, n_eval, n_donly, n_skip, n_seg = [], 0, 0, 0, 0
@@ -364,13 +373,13 @@ def main():
         b = s & 1
         buf = frames[b]
         with torch.cuda.stream(stream):
-            if world > 1 and s >= 2:
+            if gathering and s >= 2:
                 stream.wait_event(gathered[b])       # reuse buffer b only after ITS gather (step s-2)
             ev0[s].record(stream)
             M.merf_render(scene.handle, batches[s], W_IMG, H_IMG, buf, fmt=M.MERF_RGBA_U8,
                           flags=(M.MERF_TIMED if s >= args.warmup else 0) | extra_flags, stream=stream)
             ev1[s].record(stream)
-        if world > 1:
+        if gathering:
             # the gather of step s (libmerf merf_gather_frames: grouped NCCL send/recv to rank
             # 0) overlaps the render of step s+1 (the other buffer)
             gstream.wait_stream(stream)
@@ -403,12 +412,15 @@ def main():
     ms = t_start.elapsed_time(t_end)
     call_ms = [ev0[s].elapsed_time(ev1[s]) for s in range(args.warmup, steps_total)]
     gather_check = None
-    if world > 1:
+    if gathering:
         # integrity of the last gather: rank 0's slot r holds rank r's last frames
         last = (steps_total - 1) & 1
         ck = torch.tensor([float(frames[last].sum(dtype=torch.int64).item())], device=dev)
         cks = [torch.zeros_like(ck) for _ in range(world)]
-        dist.all_gather(cks, ck)
+        if world > 1:
+            dist.all_gather(cks, ck)
+        else:
+            cks = [ck]
         if rank == 0:
             got = [float(root_bufs[last][r].sum(dtype=torch.int64).item()) for r in range(world)]
             gather_check = all(abs(g - float(c.item())) == 0 for g, c in zip(got, cks))
@@ -457,7 +469,7 @@ def main():
 
     # ---- end to end through the C ABI with host buffers (pinned), copies in the timed region
     e2e = None
-    if not args.no_e2e and world > 1:
+    if not args.no_e2e and gathering:
         e2e = e2e_multi(M, scene, comm, batches, args, rank, world, dev, stream, gstream, frames, root_bufs,
                         total_rays)
     elif not args.no_e2e:
@@ -521,7 +533,7 @@ def main():
             "gather": ({"path": "libmerf merf_gather_frames (grouped ncclSend/ncclRecv to rank 0 on a side "
                                 "stream, overlapped with the next step's render)",
                         "bytes_per_step": rays_per_step * 4 * (world - 1), "verified": gather_check}
-                       if world > 1 else None),
+                       if gathering else None),
             "rank_imbalance": max(rank_ms) / (sum(rank_ms) / len(rank_ms)),
             "gather_gbs": achieved,
             "roofline": roofline,

@@ -163,3 +163,19 @@ def test_two_rank_nccl_shard_gather():
         p.join(timeout=120)
         assert p.exitcode == 0
     assert ok
+
+
+def test_bench_gather_path_one_rank():
+    """bench.py's N > 1 pipeline (frames gathered to rank 0 through merf_gather_frames, the
+    e2e leg timing render -> gather -> root D2H) run through a 1-rank communicator."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "bench.py", "--force-gather", "--steps", "2", "--warmup", "3",
+                          "--views", "2", "--no-cpu-baseline"], cwd=root, capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["gather"]["verified"] is True
+    assert "merf_gather_frames" in line["e2e"]["path"] and line["e2e"]["value"] > 0
