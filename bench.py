@@ -415,7 +415,7 @@ def main():
     if gathering:
         # integrity of the last gather: rank 0's slot r holds rank r's last frames
         last = (steps_total - 1) & 1
-        ck = torch.tensor([float(frames[last].sum(dtype=torch.int64).item())], device=dev)
+        ck = torch.tensor([float(frames[last].sum(dtype=torch.int64).item())], dtype=torch.float64, device=dev)
         cks = [torch.zeros_like(ck) for _ in range(world)]
         if world > 1:
             dist.all_gather(cks, ck)

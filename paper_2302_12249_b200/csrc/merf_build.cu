@@ -4,6 +4,7 @@
 //   and the contract_pi helper.
 #include <cstdint>
 #include <cub/device/device_scan.cuh>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "merf_device.cuh"
@@ -358,7 +359,34 @@ struct LevelSet {
 // Qa and U), the exact positions lie in [-2, 2]^3, and k < K <= 4 sqrt(3) / Delta <= 3.7e6
 // for the smallest accepted Delta = 2^-19 -- below the finest cell of 2^21 units at the
 // largest table resolution N = 512 (2^22 at N = 256).
-__global__ void skiptab_kernel(LevelSet ls, uint32_t* __restrict__ tab) {
+// Chebyshev (L-inf) distance, in finest cells, from every cell to the nearest occupied one,
+// capped at kChebCap: three separable passes (x, y, z) over byte grids, each cell scanning its
+// row outwards until the running minimum cannot improve.  dist = 0 for occupied cells.
+constexpr int kChebCap = 128;
+__global__ void cheb_pass_kernel(const uint32_t* __restrict__ occ, const uint8_t* __restrict__ src,
+                                 uint8_t* __restrict__ dst, int N, int axis) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (int64_t)N * N * N) return;
+    const int x = (int)(i % N), y = (int)((i / N) % N), z = (int)(i / ((int64_t)N * N));
+    const int c = axis == 0 ? x : (axis == 1 ? y : z);
+    const int64_t stride = axis == 0 ? 1 : (axis == 1 ? N : (int64_t)N * N);
+    int best = kChebCap;
+    if (axis == 0) {
+        for (int d = 0; d < best && d < N; d++) {          // 1D distance to an occupied cell in the row
+            if (c - d >= 0 && ((__ldg(occ + ((i - d) >> 5)) >> ((i - d) & 31)) & 1u)) { best = d; break; }
+            if (c + d < N && ((__ldg(occ + ((i + d) >> 5)) >> ((i + d) & 31)) & 1u)) { best = d; break; }
+        }
+    } else {
+        // L-inf composition: min over offsets t of max(|t|, previous distance at c + t)
+        for (int t = 0; t < best && t < N; t++) {
+            if (c - t >= 0) best = min(best, max(t, (int)src[i - t * stride]));
+            if (c + t < N) best = min(best, max(t, (int)src[i + t * stride]));
+        }
+    }
+    dst[i] = (uint8_t)best;
+}
+
+__global__ void skiptab_kernel(LevelSet ls, const uint8_t* __restrict__ cheb, uint32_t* __restrict__ tab) {
     const int nl = ls.n;
     const int N = 1 << (nl - 1);
     const int Nb = N + 2;
@@ -386,6 +414,12 @@ __global__ void skiptab_kernel(LevelSet ls, uint32_t* __restrict__ tab) {
                 }
             }
             code = (uint32_t)(kF + 2 - lev - 16);   // lattice shift of resolution 2^lev, - 16
+            // the cube of Chebyshev radius D - 1 around the cell is empty too (D = distance to
+            // the nearest occupied cell); take it when it is larger than the dyadic cell
+            if (cheb) {
+                const int r = (int)cheb[c] - 1;
+                if (2 * r + 1 > (1 << (nl - 1 - lev))) code = 128u + (uint32_t)min(r, 127);
+            }
         }
         out |= code << (8 * q);
     }
@@ -408,11 +442,27 @@ cudaError_t launch_skiptab(const uint32_t* finest, int Nf, uint32_t* tab, cudaSt
         if (e == cudaSuccess) e = launch_maxpool_bits(ls.occ[l + 1], 2 * M, tmp[l], M, st);
         ls.occ[l] = tmp[l];
     }
+    // Chebyshev distances (MERF_SKIP_DYADIC=1: dyadic cells only, the r01 table, for A/B)
+    uint8_t* dist[2] = {nullptr, nullptr};
+    const char* env = getenv("MERF_SKIP_DYADIC");
+    const bool use_cheb = !(env && env[0] == '1');
+    const int64_t cells = (int64_t)Nf * Nf * Nf;
+    if (use_cheb && e == cudaSuccess) {
+        e = cudaMallocAsync(&dist[0], cells, st);
+        if (e == cudaSuccess) e = cudaMallocAsync(&dist[1], cells, st);
+        const unsigned g = (unsigned)((cells + 255) / 256);
+        if (e == cudaSuccess) cheb_pass_kernel<<<g, 256, 0, st>>>(finest, nullptr, dist[0], Nf, 0);
+        if (e == cudaSuccess) cheb_pass_kernel<<<g, 256, 0, st>>>(finest, dist[0], dist[1], Nf, 1);
+        if (e == cudaSuccess) cheb_pass_kernel<<<g, 256, 0, st>>>(finest, dist[1], dist[0], Nf, 2);
+        if (e == cudaSuccess) e = cudaGetLastError();
+    }
     if (e == cudaSuccess) {
         const int64_t words = skiptab_words(Nf);
-        skiptab_kernel<<<(unsigned)((words + 255) / 256), 256, 0, st>>>(ls, tab);
+        skiptab_kernel<<<(unsigned)((words + 255) / 256), 256, 0, st>>>(ls, use_cheb ? dist[0] : nullptr, tab);
         e = cudaGetLastError();
     }
+    for (int q = 0; q < 2; q++)
+        if (dist[q]) cudaFreeAsync(dist[q], st);
     for (int l = 0; l < kMaxDyadic; l++)
         if (tmp[l]) cudaFreeAsync(tmp[l], st);
     return e;

@@ -941,15 +941,23 @@ __global__ void __launch_bounds__(kMarchThreads, MERF_MARCH_MINB) march_kernel(c
                 MERF_CHECK(fcell >= 0 && (int64_t)fcell < (int64_t)Nb * Nb * Nb);
                 const unsigned code = __ldg(reinterpret_cast<const uint8_t*>(S.skiptab) + (unsigned)fcell);
                 if (code == 0u) { found = true; return; }
-                const int sh = (int)code + 16;
-                const int N = 1 << (kF + 2 - sh);
-                const int cx = occ_cell(Qx, sh, N), cy = occ_cell(Qy, sh, N), cz = occ_cell(Qz, sh, N);
+                // the empty cube to leave (the larger of the two the table offers, reading D23):
+                //  code < 128: the aligned dyadic cell of lattice shift code + 16 containing the sample;
+                //  code >= 128: the cube of Chebyshev radius r = code - 128 finest cells centred on the
+                //  sample's finest cell.  Either as [lo, lo + w) per axis, lo = (Q & ~(2^a - 1)) - b.
+                const bool cheb = code >= 128u;
+                const int r = (int)code - 128;
+                const int a = cheb ? sf : (int)code + 16;
+                const int b = cheb ? (r << sf) : 0;
+                const int w = cheb ? ((2 * r + 1) << sf) : (1 << a);
+                const int msk = -(1 << a);
+                const int lx = (Qx & msk) - b, ly = (Qy & msk) - b, lz = (Qz & msk) - b;
                 // one convergent exit computation for every skipping lane: jump to the first
-                // lattice sample outside that empty cell (ray-AABB exit)
+                // lattice sample outside that empty cube (ray-AABB exit)
                 const int K = qa.w;
-                int e = min(K, exit_axis(qa.x, uu.x, cx << sh, (cx + 1) << sh, K));
-                e = min(e, exit_axis(qa.y, uu.y, cy << sh, (cy + 1) << sh, K));
-                e = min(e, exit_axis(qa.z, uu.z, cz << sh, (cz + 1) << sh, K));
+                int e = min(K, exit_axis(qa.x, uu.x, lx, lx + w, K));
+                e = min(e, exit_axis(qa.y, uu.y, ly, ly + w, K));
+                e = min(e, exit_axis(qa.z, uu.z, lz, lz + w, K));
                 k = min(max(k + 1, e), K);
                 if (KF & KF_COUNT) c_skip++;
                 return;
