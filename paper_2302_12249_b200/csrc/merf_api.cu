@@ -83,6 +83,8 @@ merf_status merf_set_error(merf_status s, const char* msg) {   // for the other 
 
 static const int kSkipTabMaxRes = 512;
 
+
+
 static bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
 static int ilog2i(int64_t v) { int n = 0; while ((int64_t(1) << n) < v) n++; return n; }
 static int64_t occ_words(int N) { return ((int64_t)N * N * N + 31) / 32; }
@@ -289,10 +291,6 @@ extern "C" merf_status merf_scene_upload(const merf_scene_desc* desc, const uint
         UP_TRY(dalloc(s, &d_pp, ppb));
         UPC_TRY(launch_pack_pairs(d_pl, desc->R, d_pp, nullptr, 0, nullptr, cs));
         S.plane_pairs = d_pp;
-        uint32_t* d_pd;
-        UP_TRY(dalloc(s, &d_pd, (size_t)3 * (desc->R + 1) * desc->R * 4));
-        UPC_TRY(launch_pack_density(d_pl, desc->R, d_pd, nullptr, 0, nullptr, cs));
-        S.pdens = d_pd;
         UPC_TRY(cudaFreeAsync(d_pl, cs));
     }
     // ---- occupancy pyramid (K0)
@@ -368,10 +366,6 @@ extern "C" merf_status merf_scene_upload(const merf_scene_desc* desc, const uint
         UP_TRY(dalloc(s, &d_ap, (size_t)n_blocks * 648 * 16));
         if (n_blocks) UPC_TRY(launch_pack_pairs(nullptr, 0, nullptr, d_at, n_blocks, d_ap, cs));
         S.atlas_pairs = d_ap;
-        uint2* d_vd;
-        UP_TRY(dalloc(s, &d_vd, (size_t)n_blocks * 512 * 8));
-        if (n_blocks) UPC_TRY(launch_pack_density(nullptr, 0, nullptr, d_at, n_blocks, d_vd, cs));
-        S.vdens = d_vd;
         if (d_at) UPC_TRY(cudaFreeAsync(d_at, cs));
     }
     UPC_TRY(cudaStreamSynchronize(cs));

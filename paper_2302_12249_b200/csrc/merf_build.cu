@@ -158,42 +158,6 @@ __global__ void contract_kernel(const double* __restrict__ x, int64_t n, double*
     if (region) region[i] = g;
 }
 
-// Density-first gather layouts (internal; built once at upload).  Plane texel (u, v) holds
-// the density bytes of its bilinear quad (u..u+1, v..v+1); a grid base voxel holds the
-// density bytes of its trilinear octet from the block's 9^3 apron storage.  One load then
-// fetches all corners of a source for the density pass (P:311 texture split).
-// density quads in the [3][R + 1][R] layout (row R of each plane repeats row R - 1)
-__global__ void pack_plane_density_kernel(const uint8_t* __restrict__ planes, int R,
-                                          uint32_t* __restrict__ pdens) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    int64_t n = (int64_t)3 * (R + 1) * R;
-    if (i >= n) return;
-    int a = (int)(i / ((int64_t)(R + 1) * R));
-    int v = min((int)((i / R) % (R + 1)), R - 1), u = (int)(i % R);
-    int u1 = min(u + 1, R - 1), v1 = min(v + 1, R - 1);
-    const uint8_t* pl = planes + (size_t)a * R * R * 8;
-    uint32_t q = (uint32_t)pl[((size_t)v * R + u) * 8] | ((uint32_t)pl[((size_t)v * R + u1) * 8] << 8) |
-                 ((uint32_t)pl[((size_t)v1 * R + u) * 8] << 16) | ((uint32_t)pl[((size_t)v1 * R + u1) * 8] << 24);
-    pdens[i] = q;
-}
-
-__global__ void pack_voxel_density_kernel(const uint8_t* __restrict__ atlas, int64_t n_blocks,
-                                          uint2* __restrict__ vdens) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n_blocks * 512) return;
-    int64_t blk = i >> 9;
-    int l = (int)(i & 511);
-    int lx = l & 7, ly = (l >> 3) & 7, lz = l >> 6;
-    const uint8_t* base = atlas + (size_t)blk * 729 * 8;
-    uint32_t w[2] = {0u, 0u};
-    for (int c = 0; c < 8; c++) {
-        int dx = c & 1, dy = (c >> 1) & 1, dz = c >> 2;
-        uint32_t b = base[(((lz + dz) * 9 + (ly + dy)) * 9 + (lx + dx)) * 8];
-        w[c >> 2] |= b << (8 * (c & 3));
-    }
-    vdens[i] = make_uint2(w[0], w[1]);
-}
-
 // NEXT-1 baking: one thread per weighted point; a point with w > w_thr and
 // tau > tau_thr (i.e. alpha = 1 - exp(-tau Delta) > 0.005 with the renderer's step)
 // marks the eight voxels around its contracted position (trilinear corners of the
@@ -304,15 +268,6 @@ cudaError_t launch_block_number(const uint8_t* need, int64_t slots, int32_t* ind
 cudaError_t launch_block_check(const uint8_t* need, const int32_t* index, int64_t slots,
                                int64_t n_blocks, unsigned long long* d_bad, cudaStream_t st) {
     block_check_kernel<<<blocks_for(slots, 256), 256, 0, st>>>(need, index, slots, n_blocks, d_bad);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_pack_density(const uint8_t* planes, int R, uint32_t* pdens, const uint8_t* atlas,
-                                int64_t n_blocks, uint2* vdens, cudaStream_t st) {
-    if (planes && R > 0)
-        pack_plane_density_kernel<<<blocks_for((int64_t)3 * (R + 1) * R, 256), 256, 0, st>>>(planes, R, pdens);
-    if (atlas && n_blocks > 0)
-        pack_voxel_density_kernel<<<blocks_for(n_blocks * 512, 256), 256, 0, st>>>(atlas, n_blocks, vdens);
     return cudaGetLastError();
 }
 

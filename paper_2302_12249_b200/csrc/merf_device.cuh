@@ -40,8 +40,6 @@ struct DevScene {
     const uint4* plane_pairs;     // [3][R + 1][R]: row R of each plane repeats row R - 1
     const int32_t* block_index;   // [(L/8)^3]
     const uint4* atlas_pairs;     // [n_blocks][9][9][8]
-    const uint32_t* pdens;        // [3][R + 1][R] density quads, byte du + 2 dv (same rows)
-    const uint2* vdens;           // [n_blocks][8][8][8] density octets, byte dx + 2 dy + 4 dz
     const uint32_t* occ[MERF_MAX_LEVELS];
     const uint32_t* occ_fin;      // = occ[n_levels - 1] (static offset: no dynamic param indexing)
     int n_fin, s_fin;             // = level_res / level_shift of the finest level

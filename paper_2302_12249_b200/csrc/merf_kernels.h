@@ -39,8 +39,6 @@ cudaError_t launch_block_number(const uint8_t* need, int64_t slots, int32_t* ind
 cudaError_t launch_block_check(const uint8_t* need, const int32_t* index, int64_t slots,
                                int64_t n_blocks, unsigned long long* d_bad, cudaStream_t st);
 // internal density-first layouts (quads per plane texel, octets per grid base voxel)
-cudaError_t launch_pack_density(const uint8_t* planes, int R, uint32_t* pdens, const uint8_t* atlas,
-                                int64_t n_blocks, uint2* vdens, cudaStream_t st);
 // NEXT-1 baking helpers
 cudaError_t launch_bake_occupancy(const double* x, const double* tau, const double* w, int64_t n,
                                   double tau_thr, double w_thr, int N, uint32_t* bits, cudaStream_t st);
