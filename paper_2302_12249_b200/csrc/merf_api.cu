@@ -609,6 +609,7 @@ static merf_status run_chunk(const merf_scene* s, int kf_setup, int kf_march, in
         return MERF_OK;
     }
     if (ws.tile_list) CUDA_TRY(cudaMemsetAsync(ws.bucket_cnt, 0, kBuckets * sizeof(unsigned int), st));
+    if (ws.tile_list && !(kf_setup & (KF_RAYS | KF_TRACE | KF_SEGS | KF_SPH))) kf_setup |= KF_LPT;
     merf_status e = timed_launch(s, flags, 0, st, call_setup, &c);
     if (e) return e;
     if (kf_march >= 0 && (e = timed_launch(s, flags, 1, st, call_march, &c))) return e;

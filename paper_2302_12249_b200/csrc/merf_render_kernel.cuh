@@ -41,6 +41,9 @@ enum : int {
                         // persistent tile-scheduled march (MERF_SPHERICAL | MERF_SPH_PERSISTENT)
     KF_FUSED = 1024,    // the deferred MLP (tensor cores) and the output store run in the march
                         // at each tile's end: no shade kernel, no accumulator round trip
+    KF_LPT = 8192,      // setup: also estimate each tile's cost and file it for longest-first
+                        // dispatch (launches of <= 4 views; a separate instance so that the
+                        // batched setup keeps its registers)
 };
 
 // The paper's default scene geometry (L = 512, R = 2048; finest occupancy level
@@ -324,7 +327,7 @@ __device__ __forceinline__ void emit_segment(const DevScene& S, int g, const dou
 }
 
 template <int KF>
-__global__ void __launch_bounds__(kSetupThreads, 7) setup_kernel(DevScene S, RaySource rs, Workspace ws,
+__global__ void __launch_bounds__(kSetupThreads, (KF & KF_LPT) ? 7 : 8) setup_kernel(DevScene S, RaySource rs, Workspace ws,
                                                               TraceArgs ta, unsigned long long* stats) {
     __shared__ double s_cand[kSetupThreads][13];   // 13: odd stride, conflict-free rows
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // index within chunk
@@ -401,7 +404,7 @@ __global__ void __launch_bounds__(kSetupThreads, 7) setup_kernel(DevScene S, Ray
         MERF_CHECK(nseg <= ws.seg_slots);        // kMaxSegCore bound (proof at kMaxSegCore)
         ws.nseg[r] = (uint8_t)min(nseg, ws.seg_slots);
     }
-    if (!(KF & (KF_SEGS | KF_TRACE | KF_SPH)) && ws.tile_list) {
+    if ((KF & KF_LPT) && !(KF & (KF_SEGS | KF_TRACE | KF_SPH))) {
         // one 32-ray tile per warp (chunks are tile aligned): file it under its cost bucket
         __syncwarp();                                  // the centre ray's segments are written
         const int b = tile_cost_bucket(S, ws, r, rs.n);

@@ -14,7 +14,9 @@ static cudaError_t setup_v(const DevScene& S, const RaySource& rs, const Workspa
 
 cudaError_t launch_setup(int kf, const DevScene& S, const RaySource& rs, const Workspace& ws,
                          const TraceArgs& ta, unsigned long long* stats, cudaStream_t st) {
-    switch (kf & (KF_RAYS | KF_TRACE | KF_SEGS | KF_COUNT | KF_SPH)) {
+    switch (kf & (KF_RAYS | KF_TRACE | KF_SEGS | KF_COUNT | KF_SPH | KF_LPT)) {
+        case KF_LPT: return setup_v<KF_LPT>(S, rs, ws, ta, stats, st);
+        case KF_LPT | KF_COUNT: return setup_v<KF_LPT | KF_COUNT>(S, rs, ws, ta, stats, st);
         case KF_SPH: return setup_v<KF_SPH>(S, rs, ws, ta, stats, st);
         case KF_SPH | KF_COUNT: return setup_v<KF_SPH | KF_COUNT>(S, rs, ws, ta, stats, st);
         case 0: return setup_v<0>(S, rs, ws, ta, stats, st);
