@@ -631,3 +631,42 @@ def test_randomised_stress_one_case_per_geometry(M):
     mod = importlib.util.module_from_spec(spec)
     spec.loader.exec_module(mod)
     assert mod.run(len(mod.GEOMS), seed=2026, verbose=False) == 0
+
+
+@pytest.mark.parametrize("cfg", ["c2", "rand"])
+def test_mixed_skip_table_equals_dyadic(M, c2, cfg):
+    """reading D23, round 2: the table offers per cell the larger of the coarsest empty dyadic
+    cell and the empty Chebyshev cube around it (MERF_SKIP_DYADIC=1 builds the dyadic-only
+    table).  Both skip only empty space: identical frames, evaluated samples and visited-cell
+    traces, and the mixed table needs fewer skips over the frame."""
+    import os
+    import torch
+    if cfg == "c2":
+        sc = c2
+        cams, W, H = config_cameras("c2")
+    else:
+        sc = random_scene(seed=12, L=64, R=128, level_res=(4, 16, 64), occ_fraction=0.05, blob_cells=3)
+        W, H = 96, 64
+        cams = look_at_camera(np.array([0.3, 1.2, -1.4]), target=np.zeros(3), W=W, H=H, fov_x_deg=80)[None]
+    pix = np.random.default_rng(4).integers(0, W * H, 300)
+    outs, stats, traces = [], [], []
+    for env in ("1", "0"):
+        os.environ["MERF_SKIP_DYADIC"] = env           # read when the scene is uploaded
+        try:
+            s = M.Scene(sc)
+        finally:
+            os.environ.pop("MERF_SKIP_DYADIC", None)
+        out, st = s.render(cams, W, H, stats=True)
+        pid = torch.as_tensor(pix, device="cuda")
+        cells = torch.zeros((len(pix), 4096), dtype=torch.int64, device="cuda")
+        cnt = torch.zeros(len(pix), dtype=torch.int32, device="cuda")
+        M.merf_trace(s.handle, cams[0], W, pid, 4096, cells, None, cnt, flags=M.MERF_NO_EARLY_TERM)
+        torch.cuda.synchronize()
+        s.close()
+        outs.append(out.cpu().numpy())
+        stats.append({k: st[k] for k in ("evaluated", "skips", "density_only")})
+        traces.append((cells.cpu().numpy(), cnt.cpu().numpy()))
+    assert np.array_equal(outs[0], outs[1])
+    assert stats[0]["evaluated"] == stats[1]["evaluated"] and stats[0]["density_only"] == stats[1]["density_only"]
+    assert stats[1]["skips"] < stats[0]["skips"]
+    assert np.array_equal(traces[0][0], traces[1][0]) and np.array_equal(traces[0][1], traces[1][1])
