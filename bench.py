@@ -473,28 +473,33 @@ def main():
         e2e = e2e_multi(M, scene, comm, batches, args, rank, world, dev, stream, gstream, frames, root_bufs,
                         total_rays)
     elif not args.no_e2e:
-        host = torch.empty((V, H_IMG, W_IMG, 4), dtype=torch.uint8).pin_memory()
+        # a frame stream through the public API: each step's views are rendered and copied to
+        # pinned host memory (merf_render_host_async: the copy of step s overlaps the render of
+        # step s + 1); the timed region ends when the last step's frames are in host memory
+        host = [torch.empty((V, H_IMG, W_IMG, 4), dtype=torch.uint8).pin_memory() for _ in range(2)]
         for s in range(min(2, args.warmup)):
-            M.merf_render_host(scene.handle, batches[s], W_IMG, H_IMG, host, fmt=M.MERF_RGBA_U8, stream=stream)
+            M.merf_render_host_async(scene.handle, batches[s], W_IMG, H_IMG, host[s & 1], fmt=M.MERF_RGBA_U8,
+                                     stream=stream)
+        M.merf_host_wait(scene.handle)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
+        t0 = time.perf_counter()
         for s in range(args.warmup, steps_total):
-            M.merf_render_host(scene.handle, batches[s], W_IMG, H_IMG, host, fmt=M.MERF_RGBA_U8, stream=stream)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        ems = e0.elapsed_time(e1)
+            M.merf_render_host_async(scene.handle, batches[s], W_IMG, H_IMG, host[s & 1], fmt=M.MERF_RGBA_U8,
+                                     stream=stream)
+        M.merf_host_wait(scene.handle)
+        ems = (time.perf_counter() - t0) * 1e3       # host clock: the frames are on the host
         if world > 1:
             t = torch.tensor([ems], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
         e2e = {"value": total_rays / (ems / 1e3), "unit": "rays/s",
                "h2d_bytes_per_step": V * 136, "d2h_bytes_per_step": V * W_IMG * H_IMG * 4,
-               "path": "merf_render_host (C ABI, pinned host output; device staging, each chunk's copy "
-                       "overlapped with the next chunk's render: chunks of 14 + 2 views)"}
+               "path": "merf_render_host_async per step (C ABI: render into a scene-owned device buffer, "
+                       "copy to pinned host memory on the scene's copy stream, overlapped with the next "
+                       "step's render) + merf_host_wait; host wall clock from the first call to the last "
+                       "frame in host memory"}
 
     if rank == 0:
         cpu = None

@@ -313,6 +313,23 @@ merf_status merf_render_host(const merf_scene *scene, const merf_camera *cams, i
                              uint32_t flags, void *stream);
 
 /*
+ * Asynchronous end-to-end variant for frame streams: renders the n_cams views into one of two
+ * scene-owned device buffers (alternating between calls) and enqueues their copy to `out_host`
+ * [host, pinned for an asynchronous copy] on the scene's copy stream; returns at once.  The
+ * next call renders into the other buffer while this copy runs, so a stream of calls keeps the
+ * GPU rendering; a call reuses a buffer only after its previous copy completed (device-side
+ * ordering, no host wait).  `out_host` must stay allocated and must not be read until
+ * merf_host_wait(scene) returns.  One host thread per scene for these calls.  Same layouts /
+ * errors as merf_render.
+ */
+merf_status merf_render_host_async(const merf_scene *scene, const merf_camera *cams, int32_t n_cams,
+                                   int32_t W, int32_t H, int32_t format, void *out_host,
+                                   uint32_t flags, void *stream);
+
+/* Wait until every copy enqueued by merf_render_host_async on `scene` has landed in host memory. */
+merf_status merf_host_wait(merf_scene *scene);
+
+/*
  * Render explicit rays: o, d [device] double [n][3] (d unit length), t_near [device] double [n]
  * or NULL (0).  rgb [device] float [n][3].  Errors: MERF_EINVAL, MERF_ECUDA.
  */

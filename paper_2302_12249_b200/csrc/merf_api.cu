@@ -34,6 +34,13 @@ struct merf_scene {
     size_t stage_bytes = 0;
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t ev[2] = {nullptr, nullptr};
+    // merf_render_host_async: two device frame buffers alternating between calls, each with
+    // the event of its last device -> host copy (on copy_stream)
+    void* astage[2] = {nullptr, nullptr};
+    size_t astage_bytes = 0;
+    int abuf = 0;
+    cudaEvent_t acopied[2] = {nullptr, nullptr};
+    bool apending[2] = {false, false};
     // MERF_TIMED bookkeeping: (kind, start, end) of launches not yet collected
     struct Timed { int kind; cudaEvent_t a, b; };
     std::mutex tmu;
@@ -221,6 +228,8 @@ extern "C" merf_status merf_scene_free(merf_scene* s) {
     for (int i = 0; i < 2; i++) {
         if (s->stage[i]) cudaFree(s->stage[i]);
         if (s->ev[i]) cudaEventDestroy(s->ev[i]);
+        if (s->astage[i]) cudaFree(s->astage[i]);
+        if (s->acopied[i]) cudaEventDestroy(s->acopied[i]);
     }
     if (s->copy_stream) cudaStreamDestroy(s->copy_stream);
     cudaSetDevice(prev);
@@ -858,6 +867,55 @@ extern "C" merf_status merf_render_host(const merf_scene* cs, const merf_camera*
     CUDA_TRY(cudaStreamSynchronize(s->copy_stream));
     CUDA_TRY(cudaStreamSynchronize(st));
     for (int i = 0; i < 2; i++) cudaEventDestroy(copied[i]);
+    return MERF_OK;
+}
+
+extern "C" merf_status merf_render_host_async(const merf_scene* cs, const merf_camera* cams, int32_t n_cams,
+                                              int32_t W, int32_t H, int32_t format, void* out_host, uint32_t flags,
+                                              void* stream) {
+    merf_status e = check_frames(cs, cams, n_cams, W, H, format, out_host);
+    if (e) return e;
+    DeviceGuard dg(cs);
+    NvtxRange nv("merf_render_host_async");
+    merf_scene* s = const_cast<merf_scene*>(cs);
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t px_bytes = format == MERF_RGBA_U8 ? 4 : 12;
+    const size_t bytes = (size_t)W * H * px_bytes * n_cams;
+    if (!s->copy_stream) CUDA_TRY(cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; i++)
+        if (!s->acopied[i]) CUDA_TRY(cudaEventCreateWithFlags(&s->acopied[i], cudaEventDisableTiming));
+    if (s->astage_bytes < bytes) {                 // grow both buffers once no copy reads them
+        CUDA_TRY(cudaStreamSynchronize(s->copy_stream));
+        for (int i = 0; i < 2; i++) {
+            if (s->astage[i]) cudaFree(s->astage[i]);
+            s->astage[i] = nullptr;
+            s->apending[i] = false;
+        }
+        s->astage_bytes = 0;
+        for (int i = 0; i < 2; i++) CUDA_TRY(cudaMalloc(&s->astage[i], bytes));
+        s->astage_bytes = bytes;
+    }
+    const int b = s->abuf;
+    s->abuf ^= 1;
+    // the render may overwrite buffer b only after ITS previous copy (two calls back) is done
+    if (s->apending[b]) CUDA_TRY(cudaStreamWaitEvent(st, s->acopied[b], 0));
+    e = render_frames(s, cams, n_cams, W, H, format, s->astage[b], flags, st, nullptr);
+    if (e) return e;
+    cudaEvent_t rendered;
+    CUDA_TRY(cudaEventCreateWithFlags(&rendered, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(rendered, st));
+    CUDA_TRY(cudaStreamWaitEvent(s->copy_stream, rendered, 0));
+    cudaEventDestroy(rendered);                    // released once the wait has been enqueued
+    CUDA_TRY(cudaMemcpyAsync(out_host, s->astage[b], bytes, cudaMemcpyDeviceToHost, s->copy_stream));
+    CUDA_TRY(cudaEventRecord(s->acopied[b], s->copy_stream));
+    s->apending[b] = true;
+    return MERF_OK;
+}
+
+extern "C" merf_status merf_host_wait(merf_scene* s) {
+    if (!s) return fail(MERF_EINVAL, "NULL scene");
+    DeviceGuard dg(s);
+    if (s->copy_stream) CUDA_TRY(cudaStreamSynchronize(s->copy_stream));
     return MERF_OK;
 }
 

@@ -113,6 +113,8 @@ SIGNATURES = [
     ("merf_scene_load", C.c_int, [C.c_char_p, _i32, C.POINTER(_vp)]),
     ("merf_cameras_read", C.c_int, [C.c_char_p, C.POINTER(merf_camera), _i32, C.POINTER(_i32), _vp, _vp]),
     ("merf_build_block_index", C.c_int, [_vp, C.POINTER(merf_scene_desc), _vp, C.POINTER(_i64), _vp]),
+    ("merf_render_host_async", C.c_int, [_vp, C.POINTER(merf_camera), _i32, _i32, _i32, _i32, _vp, _u32, _vp]),
+    ("merf_host_wait", C.c_int, [_vp]),
     ("merf_render_workspace_bytes", C.c_int, [_vp, C.POINTER(merf_camera), _i32, _i32, _i32, C.POINTER(_i64),
                                               C.POINTER(_i64)]),
     ("merf_render_shard_blocks", C.c_int, [_vp, C.POINTER(merf_camera), _i32, _i32, _i32, _i32, _i32, _i32, _vp,
@@ -353,6 +355,19 @@ class Comm:
             self.close()
         except Exception:
             pass
+
+
+def merf_render_host_async(handle, cams, W: int, H: int, out_host, fmt: int = MERF_RGBA_U8,
+                           flags: int = 0, stream=None) -> None:
+    """Render and enqueue the copy to `out_host` (pinned); returns at once (merf_host_wait)."""
+    carr = cameras_to_c(cams)
+    _check(lib().merf_render_host_async(handle, carr, len(carr), int(W), int(H), int(fmt), _ptr(out_host),
+                                        int(flags), _stream(stream)))
+
+
+def merf_host_wait(handle) -> None:
+    """Wait for every copy merf_render_host_async enqueued on this scene."""
+    _check(lib().merf_host_wait(handle))
 
 
 def merf_render_host(handle, cams, W: int, H: int, out_host, fmt: int = MERF_RGBA_U8,

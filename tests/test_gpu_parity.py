@@ -384,6 +384,23 @@ def test_render_host_equals_render(M, c1_scene):
     s.close()
 
 
+def test_render_host_async_stream_equals_render(M, c1_scene):
+    """merf_render_host_async over a stream of calls (buffers alternate, copies overlap the
+    next render, a buffer is reused only after its copy) lands every frame intact."""
+    import torch
+    s = M.Scene(c1_scene)
+    batches = [orbit_cameras(16, W=64, H=48, indices=range(i, i + 5)) for i in range(0, 15, 5)]
+    hosts = [torch.zeros((5, 48, 64, 4), dtype=torch.uint8).pin_memory() for _ in range(3)]
+    for b, h in zip(batches, hosts):
+        M.merf_render_host_async(s.handle, b, 64, 48, h, fmt=M.MERF_RGBA_U8)
+    M.merf_host_wait(s.handle)
+    for b, h in zip(batches, hosts):
+        dev = s.render(b, 64, 48, fmt=M.MERF_RGBA_U8)
+        torch.cuda.synchronize()
+        assert torch.equal(dev.cpu(), h)
+    s.close()
+
+
 def _gpu_segments(M, sc, cam, W, pixels, max_seg=8):
     import torch
     s = M.Scene(sc)
