@@ -572,6 +572,7 @@ __device__ __forceinline__ int shade_sample(const DevScene& S, int Qx, int Qy, i
             // ---- density pass, plane a: the texel quad as 2 dp2a on the .w words (c0 c0' high)
             MERF_CHECK(pi[va] >= 0 && pi[va] < R && pi[ua] >= 0 && pi[ua] < R);
             {                                            // rows v, v + 1 of the pair entries
+                MERF_CHECK((int64_t)plane_index<KF>(a, R, pi[va], pi[ua]) + R < (int64_t)3 * (R + 1) * R);
                 const uint32_t* wrow = reinterpret_cast<const uint32_t*>(S.plane_pairs + plane_index<KF>(a, R, pi[va], pi[ua]));
                 sd = __dp2a_hi(wP[a][0], __ldg(wrow + 3), sd);
                 sd = __dp2a_hi(wP[a][1], __ldg(wrow + 4 * R + 3), sd);
