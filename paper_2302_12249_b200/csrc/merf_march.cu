@@ -28,9 +28,18 @@ static cudaError_t march_v(const DevScene& S, int64_t n, const Workspace& ws, ui
     }
     int64_t need = (n + kMarchThreads - 1) / kMarchThreads;
     int grid = (int)(need < blocks ? need : blocks);
-    cudaError_t e = cudaMemsetAsync(ws.queue, 0, sizeof(unsigned int), st);
-    if (e != cudaSuccess) return e;
-    march_kernel<KF><<<grid, kMarchThreads, 0, st>>>(S, n, ws, rflags, ta, stats, rs, out);
+    // the tile queue is reset by the setup kernel that always precedes the march; launched as a
+    // programmatic dependent of it (the march waits for the setup grid with griddepcontrol.wait)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kMarchThreads);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, march_kernel<KF>, S, n, ws, rflags, ta, stats, rs, out);
     return cudaGetLastError();
 }
 

@@ -330,6 +330,11 @@ template <int KF>
 __global__ void __launch_bounds__(kSetupThreads, (KF & KF_LPT) ? 7 : 8) setup_kernel(DevScene S, RaySource rs, Workspace ws,
                                                               TraceArgs ta, unsigned long long* stats) {
     __shared__ double s_cand[kSetupThreads][13];   // 13: odd stride, conflict-free rows
+    // programmatic dependent launch: the march may be scheduled as soon as every setup CTA has
+    // started (it waits for this grid's completion before reading the workspace); the march's
+    // tile queue is reset here, so no memset sits between the two launches
+    if (blockIdx.x == 0 && threadIdx.x == 0 && ws.queue) *ws.queue = 0u;
+    asm volatile("griddepcontrol.launch_dependents;");
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // index within chunk
     const int64_t ray = rs.ray0 + r;
     bool valid = r < rs.n;
@@ -805,6 +810,10 @@ __global__ void __launch_bounds__(kMarchThreads, MERF_MARCH_MINB) march_kernel(c
                                                               unsigned long long* stats,
                                                               const __grid_constant__ RaySource rs, void* out) {
     const unsigned FULL = 0xffffffffu;
+    // programmatic dependent launch (merf_march.cu): wait for the setup grid's results; let the
+    // shade grid be scheduled behind this one
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;");
     __shared__ __align__(16) FusedSmem fsm[(KF & KF_FUSED) ? 1 : 1];
     if (KF & KF_FUSED) {
         if (threadIdx.x == 0) fsm[0].lock = 0;
@@ -1237,6 +1246,7 @@ __device__ __forceinline__ void deferred_mlp(const MlpParams& mp, const float x7
 template <int KF>
 __global__ void __launch_bounds__(kSetupThreads) shade_kernel(DevScene S, RaySource rs, Workspace ws,
                                                               void* out, const __grid_constant__ MlpParams mlp) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");    // the march's accumulators (PDL)
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= rs.n) return;
     const int64_t ray = rs.ray0 + r;

@@ -69,6 +69,7 @@ template <int KF>
 __global__ void __launch_bounds__(128) shade_mma_kernel(DevScene S, RaySource rs, Workspace ws, void* out) {
     __shared__ __align__(16) __half s_x[4][2][32][kXStride];   // [warp][hi, lo][pixel][input]
     __shared__ __align__(16) float s_o[4][32][4];               // [warp][pixel][h0 h1 h2 -]
+    asm volatile("griddepcontrol.wait;" ::: "memory");    // the march's accumulators (PDL)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // index within chunk
     const int64_t ray = rs.ray0 + r;
@@ -246,7 +247,16 @@ static cudaError_t shade_mma_v(const DevScene& S, const RaySource& rs, const Wor
                                cudaStream_t st) {
     if (rs.n <= 0) return cudaSuccess;
     dim3 grid((unsigned)((rs.n + 127) / 128));
-    shade_mma_kernel<KF><<<grid, 128, 0, st>>>(S, rs, ws, out);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(128);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // behind the march (PDL)
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, shade_mma_kernel<KF>, S, rs, ws, out);
     return cudaGetLastError();
 }
 
