@@ -488,14 +488,13 @@ static int seg_slots_for(const merf_camera* cams, int n) {
     return kMaxSegCore;
 }
 
-// Tile dispatch order.  Cost-ordered (longest first, Workspace::tile_list) for launches of at
-// most kLptMaxViews views, raster order otherwise.  Measured on 1080p orbit views (bench
-// workload, tools/view_scaling.py): the march's tail (tile queue dry -> last warp exit) drops
-// from 0.36-0.47 ms to 0.10-0.17 ms for 2-16 views and the march per view by 1-6 %, but the
-// estimate costs 0.035-0.04 ms of setup per view, so it pays only while the tail is a large
-// share of the launch (1-4 views: 1.8 % to 6 % faster per view); at 16 views it is a 2 % loss.
-// MERF_TILE_ORDER=raster / cost forces either order (A/B).
-static const int kLptMaxViews = 4;
+// Tile dispatch order: raster by default; cost-ordered (longest first, Workspace::tile_list)
+// with MERF_TILE_ORDER=cost.  Measured on 1080p orbit views (tools/view_scaling.py, r02 final
+// kernels): the march's tail (tile queue dry -> last warp exit) drops from 0.33-0.45 ms to
+// 0.09-0.29 ms and the march per view by 0.5-3 %, but the estimate adds 0.05 ms of setup per
+// view, so the call is 0.5-3 % slower at every batch size from 1 to 16 views.  (An earlier
+// policy used it for <= 4 views on a measurement that predates the setup-instance split.)
+static const int kLptMaxViews = 0;
 static bool fused_mlp() {
     static const bool v = [] { const char* e = getenv("MERF_FUSED_MLP"); return e && e[0] == '1'; }();
     return v;
@@ -610,6 +609,8 @@ static merf_status run_chunk(const merf_scene* s, int kf_setup, int kf_march, in
         if (kf_march >= 0) kf_march = KF_SPH | (kf_march & KF_COUNT);
         flags &= ~(uint32_t)MERF_SPHERICAL;
     }
+    // longest-first dispatch: the setup instance that also files every tile under its cost bucket
+    if (ws.tile_list && !(kf_setup & (KF_RAYS | KF_TRACE | KF_SEGS | KF_SPH))) kf_setup |= KF_LPT;
     ChunkCall c{s, kf_setup, kf_march, kf_shade, &rs, &ws, out, flags, &ta, d_stats, st};
     if (flags & MERF_SPHERICAL) {          // NEXT-2 variant: no setup kernel, one march kernel
         merf_status e = timed_launch(s, flags, 1, st, call_march_sph, &c);
@@ -618,7 +619,6 @@ static merf_status run_chunk(const merf_scene* s, int kf_setup, int kf_march, in
         return MERF_OK;
     }
     if (ws.tile_list) CUDA_TRY(cudaMemsetAsync(ws.bucket_cnt, 0, kBuckets * sizeof(unsigned int), st));
-    if (ws.tile_list && !(kf_setup & (KF_RAYS | KF_TRACE | KF_SEGS | KF_SPH))) kf_setup |= KF_LPT;
     merf_status e = timed_launch(s, flags, 0, st, call_setup, &c);
     if (e) return e;
     if (kf_march >= 0 && (e = timed_launch(s, flags, 1, st, call_march, &c))) return e;

@@ -171,10 +171,11 @@ __device__ __forceinline__ int64_t out_index(const RaySource& rs, int view, int 
 // tail -- from the moment its tile queue runs dry to the last warp's exit -- is the duration
 // of the most expensive tiles taken last (measured 0.36-0.47 ms per launch on the orbit views,
 // 23 % of a single 1080p view: 1 % of the tiles have a ray with >= 268 evaluated samples, 5x the
-// median tile, and take ~1 ms under full load).  The setup kernel therefore estimates every
-// 32-ray tile's cost (tile_cost_bucket) and appends the tile to one of kBuckets lists by log2 of
-// the estimate; the march takes the lists most expensive first.  The order changes no ray's
-// arithmetic: every tile is still marched by one warp.
+// median tile, and take ~1 ms under full load).  With MERF_TILE_ORDER=cost the setup kernel
+// estimates every 32-ray tile's cost (tile_cost_bucket) and appends the tile to one of kBuckets
+// lists by log2 of the estimate; the march takes the lists most expensive first.  The order
+// changes no ray's arithmetic: every tile is still marched by one warp.  Measured a net loss
+// (the estimate costs more setup time than the shorter tail saves), so raster is the default.
 constexpr int kBuckets = 8;
 
 struct Workspace {
