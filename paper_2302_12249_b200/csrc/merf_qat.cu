@@ -266,6 +266,33 @@ __global__ void __launch_bounds__(128) qat_bwd_kernel(RaySource rs, QatArgs A, c
     for (int c = 0; c < 7; c++) G[c] = row[9 + c];
     const float* rec0 = A.samp + (size_t)r * A.smax * 12;
     float Rt[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    // Run merging for the 3D grid: consecutive samples of a ray usually share their V cell (8
+    // lattice steps per voxel at L = 128), so the 8 corners' gradients are summed in registers
+    // while the cell stays the same and reduced to memory once per run (16 red.v4 per run
+    // instead of per sample).  The reductions are the kernel's bound (L2 reduction units,
+    // conflicts between a ray's consecutive samples), DESIGN.md NEXT-3.
+    float vacc[8][8];
+#pragma unroll
+    for (int c = 0; c < 8; c++)
+#pragma unroll
+        for (int q = 0; q < 8; q++) vacc[c][q] = 0.f;
+    int cur_e0 = -1;
+    unsigned touched = 0u;
+    auto flush_v = [&]() {
+        if (cur_e0 < 0) return;
+#pragma unroll
+        for (int c = 0; c < 8; c++) {
+            if (touched & (1u << c)) {
+                const int dx = c & 1, dy = (c >> 1) & 1, dz = c >> 2;
+                float4* dst = reinterpret_cast<float4*>(A.gv + (size_t)(cur_e0 + (dz * A.L + dy) * A.L + dx) * 8);
+                atomicAdd(dst, make_float4(vacc[c][0], vacc[c][1], vacc[c][2], vacc[c][3]));
+                atomicAdd(dst + 1, make_float4(vacc[c][4], vacc[c][5], vacc[c][6], vacc[c][7]));
+            }
+#pragma unroll
+            for (int q = 0; q < 8; q++) vacc[c][q] = 0.f;
+        }
+        touched = 0u;
+    };
     for (int i = n - 1; i >= 0; i--) {
         const float4* rec4 = reinterpret_cast<const float4*>(rec0 + (size_t)i * 12);
         const float4 r0 = rec4[0], r1 = rec4[1], r2 = rec4[2];
@@ -287,15 +314,49 @@ __global__ void __launch_bounds__(128) qat_bwd_kernel(RaySource rs, QatArgs A, c
         const float w = alpha * Ti;
 #pragma unroll
         for (int c = 0; c < 7; c++) dt[1 + c] = w * G[c] * xs[c] * (1.f - xs[c]);
-        for_corners(A, __float_as_int(r0.x), __float_as_int(r0.y), __float_as_int(r0.z), [&](int g, int e, float wc) {
-            if (wc == 0.f) return;
-            float4* dst = reinterpret_cast<float4*>(
-                (g == 0) ? A.gv + (size_t)e * 8 : A.gp + ((size_t)(g - 1) * A.R * A.R + e) * 8);
-            // vector reductions (sm_90+): 2 per corner instead of 8 scalar atomics
-            atomicAdd(dst, make_float4(wc * dt[0], wc * dt[1], wc * dt[2], wc * dt[3]));
-            atomicAdd(dst + 1, make_float4(wc * dt[4], wc * dt[5], wc * dt[6], wc * dt[7]));
-        });
+        const int Q[3] = {__float_as_int(r0.x), __float_as_int(r0.y), __float_as_int(r0.z)};
+        {
+            int vi[3];
+            float vf[3];
+#pragma unroll
+            for (int a = 0; a < 3; a++) coord_qat(Q[a], A.L, vi[a], vf[a]);
+            const int e0 = (vi[2] * A.L + vi[1]) * A.L + vi[0];
+            if (e0 != cur_e0) {
+                flush_v();
+                cur_e0 = e0;
+            }
+#pragma unroll
+            for (int c = 0; c < 8; c++) {
+                const int dx = c & 1, dy = (c >> 1) & 1, dz = c >> 2;
+                const float wc = (dx ? vf[0] : 1.f - vf[0]) * (dy ? vf[1] : 1.f - vf[1]) * (dz ? vf[2] : 1.f - vf[2]);
+                touched |= (wc != 0.f ? 1u : 0u) << c;
+#pragma unroll
+                for (int q = 0; q < 8; q++) vacc[c][q] = fmaf(wc, dt[q], vacc[c][q]);
+            }
+        }
+        {
+            int pi[3];
+            float pf[3];
+#pragma unroll
+            for (int a = 0; a < 3; a++) coord_qat(Q[a], A.R, pi[a], pf[a]);
+#pragma unroll
+            for (int a = 0; a < 3; a++) {
+                const int ua = (a == 0) ? 1 : 0, va = (a == 2) ? 1 : 2;
+#pragma unroll
+                for (int c = 0; c < 4; c++) {
+                    const int du = c & 1, dv = c >> 1;
+                    const float wc = (du ? pf[ua] : 1.f - pf[ua]) * (dv ? pf[va] : 1.f - pf[va]);
+                    if (wc == 0.f) continue;
+                    float4* dst = reinterpret_cast<float4*>(
+                        A.gp + ((size_t)a * A.R * A.R + (pi[va] + dv) * A.R + (pi[ua] + du)) * 8);
+                    // vector reductions (sm_90+): 2 per corner instead of 8 scalar atomics
+                    atomicAdd(dst, make_float4(wc * dt[0], wc * dt[1], wc * dt[2], wc * dt[3]));
+                    atomicAdd(dst + 1, make_float4(wc * dt[4], wc * dt[5], wc * dt[6], wc * dt[7]));
+                }
+            }
+        }
     }
+    flush_v();
 }
 
 static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
