@@ -48,36 +48,6 @@ __device__ __forceinline__ void coord_qat(int Q, int M, int& i0, float& f) {
     f = fr;
 }
 
-// visit the 8 + 12 corners of lattice point Q: fn(grid (0 = V, 1..3 = plane), element, weight)
-template <typename Fn>
-__device__ __forceinline__ void for_corners(const QatArgs& A, int Qx, int Qy, int Qz, Fn fn) {
-    const int Q[3] = {Qx, Qy, Qz};
-    int vi[3];
-    float vf[3];
-#pragma unroll
-    for (int a = 0; a < 3; a++) coord_qat(Q[a], A.L, vi[a], vf[a]);
-#pragma unroll
-    for (int c = 0; c < 8; c++) {
-        const int dx = c & 1, dy = (c >> 1) & 1, dz = c >> 2;
-        const float w = (dx ? vf[0] : 1.f - vf[0]) * (dy ? vf[1] : 1.f - vf[1]) * (dz ? vf[2] : 1.f - vf[2]);
-        fn(0, ((vi[2] + dz) * A.L + (vi[1] + dy)) * A.L + (vi[0] + dx), w);
-    }
-    int pi[3];
-    float pf[3];
-#pragma unroll
-    for (int a = 0; a < 3; a++) coord_qat(Q[a], A.R, pi[a], pf[a]);
-#pragma unroll
-    for (int a = 0; a < 3; a++) {
-        const int ua = (a == 0) ? 1 : 0, va = (a == 2) ? 1 : 2;
-#pragma unroll
-        for (int c = 0; c < 4; c++) {
-            const int du = c & 1, dv = c >> 1;
-            const float w = (du ? pf[ua] : 1.f - pf[ua]) * (dv ? pf[va] : 1.f - pf[va]);
-            fn(1 + a, (pi[va] + dv) * A.R + (pi[ua] + du), w);
-        }
-    }
-}
-
 __global__ void prequant_kernel(const float* __restrict__ theta, int64_t n, int quant, float md, float ma,
                                 float* __restrict__ v) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -112,6 +82,8 @@ __global__ void __launch_bounds__(128) qat_fwd_kernel(RaySource rs, Workspace ws
     float T = 1.f;
     int n = 0;
     bool over = false;
+    float vc[8][8];                    // the current V cell's corner values
+    int cur_e0 = -1;
     const int ns = ws.nseg[r];
     for (int j = 0; j < ns; j++) {
         const int4 qa = ws.seg[(r * ws.seg_slots + j) * 2], uu = ws.seg[(r * ws.seg_slots + j) * 2 + 1];
@@ -120,19 +92,61 @@ __global__ void __launch_bounds__(128) qat_fwd_kernel(RaySource rs, Workspace ws
             if (!occ_bit(A.occf, occ_cell(Qx, A.sf, A.Nf), occ_cell(Qy, A.sf, A.Nf), occ_cell(Qz, A.sf, A.Nf), A.Nf))
                 continue;
             float t[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-            for_corners(A, Qx, Qy, Qz, [&](int g, int e, float w) {
-                const float4* src = reinterpret_cast<const float4*>(
-                    (g == 0) ? A.vv + (size_t)e * 8 : A.vp + ((size_t)(g - 1) * A.R * A.R + e) * 8);
-                const float4 a = __ldg(src), b = __ldg(src + 1);
-                t[0] = fmaf(w, a.x, t[0]);
-                t[1] = fmaf(w, a.y, t[1]);
-                t[2] = fmaf(w, a.z, t[2]);
-                t[3] = fmaf(w, a.w, t[3]);
-                t[4] = fmaf(w, b.x, t[4]);
-                t[5] = fmaf(w, b.y, t[5]);
-                t[6] = fmaf(w, b.z, t[6]);
-                t[7] = fmaf(w, b.w, t[7]);
-            });
+            // V: the 8 corners' values are kept in registers for the run of samples that
+            // share the V cell (8 lattice steps per voxel at L = 128), reloaded when it changes
+            {
+                int vi[3];
+                float vf[3];
+                coord_qat(Qx, A.L, vi[0], vf[0]);
+                coord_qat(Qy, A.L, vi[1], vf[1]);
+                coord_qat(Qz, A.L, vi[2], vf[2]);
+                const int e0 = (vi[2] * A.L + vi[1]) * A.L + vi[0];
+                if (e0 != cur_e0) {
+                    cur_e0 = e0;
+#pragma unroll
+                    for (int c = 0; c < 8; c++) {
+                        const int dx = c & 1, dy = (c >> 1) & 1, dz = c >> 2;
+                        const float4* src = reinterpret_cast<const float4*>(A.vv + (size_t)(e0 + (dz * A.L + dy) * A.L + dx) * 8);
+                        const float4 a = __ldg(src), b = __ldg(src + 1);
+                        vc[c][0] = a.x; vc[c][1] = a.y; vc[c][2] = a.z; vc[c][3] = a.w;
+                        vc[c][4] = b.x; vc[c][5] = b.y; vc[c][6] = b.z; vc[c][7] = b.w;
+                    }
+                }
+#pragma unroll
+                for (int c = 0; c < 8; c++) {
+                    const int dx = c & 1, dy = (c >> 1) & 1, dz = c >> 2;
+                    const float w = (dx ? vf[0] : 1.f - vf[0]) * (dy ? vf[1] : 1.f - vf[1]) * (dz ? vf[2] : 1.f - vf[2]);
+#pragma unroll
+                    for (int q = 0; q < 8; q++) t[q] = fmaf(w, vc[c][q], t[q]);
+                }
+            }
+            {
+                int pi[3];
+                float pf[3];
+                coord_qat(Qx, A.R, pi[0], pf[0]);
+                coord_qat(Qy, A.R, pi[1], pf[1]);
+                coord_qat(Qz, A.R, pi[2], pf[2]);
+#pragma unroll
+                for (int a = 0; a < 3; a++) {
+                    const int ua = (a == 0) ? 1 : 0, va = (a == 2) ? 1 : 2;
+#pragma unroll
+                    for (int c = 0; c < 4; c++) {
+                        const int du = c & 1, dv = c >> 1;
+                        const float w = (du ? pf[ua] : 1.f - pf[ua]) * (dv ? pf[va] : 1.f - pf[va]);
+                        const float4* src = reinterpret_cast<const float4*>(
+                            A.vp + ((size_t)a * A.R * A.R + (pi[va] + dv) * A.R + (pi[ua] + du)) * 8);
+                        const float4 a4 = __ldg(src), b4 = __ldg(src + 1);
+                        t[0] = fmaf(w, a4.x, t[0]);
+                        t[1] = fmaf(w, a4.y, t[1]);
+                        t[2] = fmaf(w, a4.z, t[2]);
+                        t[3] = fmaf(w, a4.w, t[3]);
+                        t[4] = fmaf(w, b4.x, t[4]);
+                        t[5] = fmaf(w, b4.y, t[5]);
+                        t[6] = fmaf(w, b4.z, t[6]);
+                        t[7] = fmaf(w, b4.w, t[7]);
+                    }
+                }
+            }
             const float tau = expf(t[0]);
             const float alpha = 1.f - expf(-tau * A.step);
             float xs[7];
