@@ -280,11 +280,13 @@ __global__ void __launch_bounds__(128) qat_bwd_kernel(RaySource rs, QatArgs A, c
     for (int c = 0; c < 7; c++) G[c] = row[9 + c];
     const float* rec0 = A.samp + (size_t)r * A.smax * 12;
     float Rt[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    // Run merging for the 3D grid: consecutive samples of a ray usually share their V cell (8
-    // lattice steps per voxel at L = 128), so the 8 corners' gradients are summed in registers
-    // while the cell stays the same and reduced to memory once per run (16 red.v4 per run
-    // instead of per sample).  The reductions are the kernel's bound (L2 reduction units,
-    // conflicts between a ray's consecutive samples), DESIGN.md NEXT-3.
+    // Run merging: consecutive samples of a ray usually share their V cell (8 lattice steps per
+    // voxel at L = 128) and each plane's texel cell (~2 steps at R = 4L, longer for the plane
+    // facing the ray), so the corners' gradients are summed in registers while a cell stays the
+    // same and reduced to memory once per run (2 red.v4 per corner per run instead of per
+    // sample).  The reductions are the kernel's bound (L2 reduction units, conflicts between a
+    // ray's consecutive samples), DESIGN.md NEXT-3.  (8 + 12 corners x 8 channels = 160 fp32
+    // accumulators: 226 registers, no spills; fewer resident warps, far fewer reductions.)
     float vacc[8][8];
 #pragma unroll
     for (int c = 0; c < 8; c++)
@@ -306,6 +308,31 @@ __global__ void __launch_bounds__(128) qat_bwd_kernel(RaySource rs, QatArgs A, c
             for (int q = 0; q < 8; q++) vacc[c][q] = 0.f;
         }
         touched = 0u;
+    };
+    float pacc[3][4][8];
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+#pragma unroll
+        for (int c = 0; c < 4; c++)
+#pragma unroll
+            for (int q = 0; q < 8; q++) pacc[a][c][q] = 0.f;
+    int cur_p[3] = {-1, -1, -1};
+    unsigned ptouched = 0u;
+    auto flush_p = [&](int a) {
+        if (cur_p[a] < 0) return;
+        const int pu = cur_p[a] % A.R, pv = cur_p[a] / A.R;
+#pragma unroll
+        for (int c = 0; c < 4; c++) {
+            if (ptouched & (1u << (4 * a + c))) {
+                const int du = c & 1, dv = c >> 1;
+                float4* dst = reinterpret_cast<float4*>(A.gp + ((size_t)a * A.R * A.R + (pv + dv) * A.R + (pu + du)) * 8);
+                atomicAdd(dst, make_float4(pacc[a][c][0], pacc[a][c][1], pacc[a][c][2], pacc[a][c][3]));
+                atomicAdd(dst + 1, make_float4(pacc[a][c][4], pacc[a][c][5], pacc[a][c][6], pacc[a][c][7]));
+            }
+#pragma unroll
+            for (int q = 0; q < 8; q++) pacc[a][c][q] = 0.f;
+        }
+        ptouched &= ~(15u << (4 * a));
     };
     for (int i = n - 1; i >= 0; i--) {
         const float4* rec4 = reinterpret_cast<const float4*>(rec0 + (size_t)i * 12);
@@ -356,21 +383,25 @@ __global__ void __launch_bounds__(128) qat_bwd_kernel(RaySource rs, QatArgs A, c
 #pragma unroll
             for (int a = 0; a < 3; a++) {
                 const int ua = (a == 0) ? 1 : 0, va = (a == 2) ? 1 : 2;
+                const int e = pi[va] * A.R + pi[ua];
+                if (e != cur_p[a]) {
+                    flush_p(a);
+                    cur_p[a] = e;
+                }
 #pragma unroll
                 for (int c = 0; c < 4; c++) {
                     const int du = c & 1, dv = c >> 1;
                     const float wc = (du ? pf[ua] : 1.f - pf[ua]) * (dv ? pf[va] : 1.f - pf[va]);
-                    if (wc == 0.f) continue;
-                    float4* dst = reinterpret_cast<float4*>(
-                        A.gp + ((size_t)a * A.R * A.R + (pi[va] + dv) * A.R + (pi[ua] + du)) * 8);
-                    // vector reductions (sm_90+): 2 per corner instead of 8 scalar atomics
-                    atomicAdd(dst, make_float4(wc * dt[0], wc * dt[1], wc * dt[2], wc * dt[3]));
-                    atomicAdd(dst + 1, make_float4(wc * dt[4], wc * dt[5], wc * dt[6], wc * dt[7]));
+                    ptouched |= (wc != 0.f ? 1u : 0u) << (4 * a + c);
+#pragma unroll
+                    for (int q = 0; q < 8; q++) pacc[a][c][q] = fmaf(wc, dt[q], pacc[a][c][q]);
                 }
             }
         }
     }
     flush_v();
+#pragma unroll
+    for (int a = 0; a < 3; a++) flush_p(a);
 }
 
 static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
