@@ -84,6 +84,8 @@ __global__ void __launch_bounds__(128) qat_fwd_kernel(RaySource rs, Workspace ws
     bool over = false;
     float vc[8][8];                    // the current V cell's corner values
     int cur_e0 = -1;
+    float pc[3][4][8];                 // the current plane cells' corner values
+    int cur_p[3] = {-1, -1, -1};
     const int ns = ws.nseg[r];
     for (int j = 0; j < ns; j++) {
         const int4 qa = ws.seg[(r * ws.seg_slots + j) * 2], uu = ws.seg[(r * ws.seg_slots + j) * 2 + 1];
@@ -92,8 +94,9 @@ __global__ void __launch_bounds__(128) qat_fwd_kernel(RaySource rs, Workspace ws
             if (!occ_bit(A.occf, occ_cell(Qx, A.sf, A.Nf), occ_cell(Qy, A.sf, A.Nf), occ_cell(Qz, A.sf, A.Nf), A.Nf))
                 continue;
             float t[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-            // V: the 8 corners' values are kept in registers for the run of samples that
-            // share the V cell (8 lattice steps per voxel at L = 128), reloaded when it changes
+            // V and each plane: the corners' values are kept in registers for the run of
+            // samples that share that source's cell (8 lattice steps per voxel at L = 128, ~2
+            // per plane texel), reloaded when it changes (247 registers, no spills)
             {
                 int vi[3];
                 float vf[3];
@@ -129,21 +132,25 @@ __global__ void __launch_bounds__(128) qat_fwd_kernel(RaySource rs, Workspace ws
 #pragma unroll
                 for (int a = 0; a < 3; a++) {
                     const int ua = (a == 0) ? 1 : 0, va = (a == 2) ? 1 : 2;
+                    const int e = pi[va] * A.R + pi[ua];
+                    if (e != cur_p[a]) {
+                        cur_p[a] = e;
+#pragma unroll
+                        for (int c = 0; c < 4; c++) {
+                            const int du = c & 1, dv = c >> 1;
+                            const float4* src = reinterpret_cast<const float4*>(
+                                A.vp + ((size_t)a * A.R * A.R + (pi[va] + dv) * A.R + (pi[ua] + du)) * 8);
+                            const float4 a4 = __ldg(src), b4 = __ldg(src + 1);
+                            pc[a][c][0] = a4.x; pc[a][c][1] = a4.y; pc[a][c][2] = a4.z; pc[a][c][3] = a4.w;
+                            pc[a][c][4] = b4.x; pc[a][c][5] = b4.y; pc[a][c][6] = b4.z; pc[a][c][7] = b4.w;
+                        }
+                    }
 #pragma unroll
                     for (int c = 0; c < 4; c++) {
                         const int du = c & 1, dv = c >> 1;
                         const float w = (du ? pf[ua] : 1.f - pf[ua]) * (dv ? pf[va] : 1.f - pf[va]);
-                        const float4* src = reinterpret_cast<const float4*>(
-                            A.vp + ((size_t)a * A.R * A.R + (pi[va] + dv) * A.R + (pi[ua] + du)) * 8);
-                        const float4 a4 = __ldg(src), b4 = __ldg(src + 1);
-                        t[0] = fmaf(w, a4.x, t[0]);
-                        t[1] = fmaf(w, a4.y, t[1]);
-                        t[2] = fmaf(w, a4.z, t[2]);
-                        t[3] = fmaf(w, a4.w, t[3]);
-                        t[4] = fmaf(w, b4.x, t[4]);
-                        t[5] = fmaf(w, b4.y, t[5]);
-                        t[6] = fmaf(w, b4.z, t[6]);
-                        t[7] = fmaf(w, b4.w, t[7]);
+#pragma unroll
+                        for (int q = 0; q < 8; q++) t[q] = fmaf(w, pc[a][c][q], t[q]);
                     }
                 }
             }
