@@ -89,10 +89,23 @@ __global__ void __launch_bounds__(128) qat_fwd_kernel(RaySource rs, Workspace ws
     const int ns = ws.nseg[r];
     for (int j = 0; j < ns; j++) {
         const int4 qa = ws.seg[(r * ws.seg_slots + j) * 2], uu = ws.seg[(r * ws.seg_slots + j) * 2 + 1];
-        for (int k = 0; k < qa.w; k++) {
+        const int K = qa.w;
+        for (int k = 0; k < K; k++) {
             const int Qx = qa.x + k * uu.x, Qy = qa.y + k * uu.y, Qz = qa.z + k * uu.z;
-            if (!occ_bit(A.occf, occ_cell(Qx, A.sf, A.Nf), occ_cell(Qy, A.sf, A.Nf), occ_cell(Qz, A.sf, A.Nf), A.Nf))
+            const int cx = occ_cell(Qx, A.sf, A.Nf), cy = occ_cell(Qy, A.sf, A.Nf), cz = occ_cell(Qz, A.sf, A.Nf);
+            if (!occ_bit(A.occf, cx, cy, cz, A.Nf)) {
+                // empty finest cell: jump to the first lattice sample outside it (the render
+                // march's lattice-snapped exit) -- the same evaluated-sample set as
+                // testing every step; only when the sample lies inside the (unclamped) cell
+                const int w = 1 << A.sf, lx = cx << A.sf, ly = cy << A.sf, lz = cz << A.sf;
+                if (Qx >= lx && Qx < lx + w && Qy >= ly && Qy < ly + w && Qz >= lz && Qz < lz + w) {
+                    int e = min(K, exit_axis(qa.x, uu.x, lx, lx + w, K));
+                    e = min(e, exit_axis(qa.y, uu.y, ly, ly + w, K));
+                    e = min(e, exit_axis(qa.z, uu.z, lz, lz + w, K));
+                    k = max(k, e - 1);                     // the loop's k++ lands on e
+                }
                 continue;
+            }
             float t[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
             // V and each plane: the corners' values are kept in registers for the run of
             // samples that share that source's cell (8 lattice steps per voxel at L = 128, ~2
