@@ -41,6 +41,13 @@ struct merf_scene {
     int abuf = 0;
     cudaEvent_t acopied[2] = {nullptr, nullptr};
     bool apending[2] = {false, false};
+    // per-tile march durations of the last single-chunk small call (Workspace::tile_cost):
+    // the next call with the same W, H and views dispatches its tiles longest first
+    uint16_t* hist = nullptr;
+    int64_t hist_cap = 0;
+    int hist_W = 0, hist_H = 0, hist_views = 0;
+    bool hist_valid = false;
+    std::mutex hmu;
     // MERF_TIMED bookkeeping: (kind, start, end) of launches not yet collected
     struct Timed { int kind; cudaEvent_t a, b; };
     std::mutex tmu;
@@ -231,6 +238,7 @@ extern "C" merf_status merf_scene_free(merf_scene* s) {
         if (s->astage[i]) cudaFree(s->astage[i]);
         if (s->acopied[i]) cudaEventDestroy(s->acopied[i]);
     }
+    if (s->hist) cudaFree(s->hist);
     if (s->copy_stream) cudaStreamDestroy(s->copy_stream);
     cudaSetDevice(prev);
     delete s;
@@ -488,13 +496,18 @@ static int seg_slots_for(const merf_camera* cams, int n) {
     return kMaxSegCore;
 }
 
-// Tile dispatch order: raster by default; cost-ordered (longest first, Workspace::tile_list)
-// with MERF_TILE_ORDER=cost.  Measured on 1080p orbit views (tools/view_scaling.py, r02 final
+// Tile dispatch order.  Single-chunk calls of at most kHistMaxViews views keep the march's
+// per-tile durations in the scene (Workspace::tile_cost); the next such call with the same W, H
+// and views -- the next frame of a sequence -- dispatches its tiles longest first by them
+// (exact costs of the previous frame: its heaviest tiles start at once instead of at 65 % of
+// the queue).  MERF_TILE_ORDER=raster turns this off; MERF_TILE_ORDER=cost uses the
+// centre-ray probe estimate (below) for every call instead.  Otherwise raster order.  Measured on 1080p orbit views (tools/view_scaling.py, r02 final
 // kernels): the march's tail (tile queue dry -> last warp exit) drops from 0.33-0.45 ms to
 // 0.09-0.29 ms and the march per view by 0.5-3 %, but the estimate adds 0.05 ms of setup per
 // view, so the call is 0.5-3 % slower at every batch size from 1 to 16 views.  (An earlier
 // policy used it for <= 4 views on a measurement that predates the setup-instance split.)
 static const int kLptMaxViews = 0;
+static const int kHistMaxViews = 8;
 static bool fused_mlp() {
     static const bool v = [] { const char* e = getenv("MERF_FUSED_MLP"); return e && e[0] == '1'; }();
     return v;
@@ -530,6 +543,7 @@ static merf_status ws_alloc(int64_t n, cudaStream_t st, Workspace& ws, void** ba
     ws.bucket_cnt = (unsigned int*)(b + seg + ns + acc + 128);
     ws.tile_list = (int*)(b + seg + ns + acc + 256);   // cost order available; the caller may clear it
     ws.n_tiles = (int)ws_tiles(n);
+    ws.tile_cost = nullptr;
     return MERF_OK;
 }
 
@@ -697,7 +711,36 @@ static merf_status render_frames(const merf_scene* s, const merf_camera* cams, i
     void* base = nullptr;
     merf_status e = ws_alloc(rays_per_view * vpc, st, ws, &base, seg_slots_for(cams, n_cams));
     if (e) return e;
+    int* const lists = ws.tile_list;
     if (!cost_order(vpc)) ws.tile_list = nullptr;
+    // frame-sequence history (see kHistMaxViews): one chunk, small, full frames
+    if (tile_order_override() == 0 && n_cams <= vpc && vpc <= kHistMaxViews && !prog && !shard) {
+        merf_scene* ms = const_cast<merf_scene*>(s);
+        std::lock_guard<std::mutex> g(ms->hmu);
+        const int64_t nt = (int64_t)ws_tiles(rays_per_view * n_cams);
+        if (ms->hist_cap < nt) {
+            if (ms->hist) {
+                cudaError_t ce = cudaFree(ms->hist);   // (synchronises: no launch still uses it)
+                if (ce != cudaSuccess) { cudaFreeAsync(base, st); return fail(MERF_ECUDA, "%s", cudaGetErrorString(ce)); }
+            }
+            ms->hist = nullptr;
+            ms->hist_cap = 0;
+            ms->hist_valid = false;
+            if (cudaMalloc(&ms->hist, (size_t)nt * sizeof(uint16_t)) != cudaSuccess) {
+                ms->hist = nullptr;
+                cudaFreeAsync(base, st);
+                return fail(MERF_ENOMEM, "tile-cost history allocation failed");
+            }
+            ms->hist_cap = nt;
+        }
+        const bool match = ms->hist_valid && ms->hist_W == W && ms->hist_H == H && ms->hist_views == n_cams;
+        ws.tile_cost = ms->hist;
+        ws.tile_list = match ? lists : nullptr;     // cost-ordered lists, else raster (recording)
+        ms->hist_W = W;
+        ms->hist_H = H;
+        ms->hist_views = n_cams;
+        ms->hist_valid = true;           // the march below records every tile (stream order)
+    }
     const bool count = d_stats != nullptr;
     for (int c0 = 0; c0 < n_cams; c0 += vpc) {
         const int nv = n_cams - c0 < vpc ? n_cams - c0 : vpc;

@@ -187,6 +187,10 @@ struct Workspace {
     int* tile_list;              // [kBuckets][n_tiles] tile indices, or NULL: raster order
     unsigned int* bucket_cnt;    // [kBuckets] tiles per list (zeroed before the setup)
     int n_tiles;                 // ceil(n / 32) of the current chunk
+    // per-tile march durations of the previous call with the same tiling (SM clock >> 8,
+    // saturated), or NULL.  The setup's KF_LPT path files tiles by these instead of the probe
+    // estimate; the march overwrites them with this call's durations.  Scheduling only.
+    uint16_t* tile_cost;
 };
 
 
@@ -195,6 +199,12 @@ struct Workspace {
 // 16 = first warp start, 17 = first warp to find the tile queue empty, 18 = last warp exit
 // (%globaltimer ns, min/min/max), folded into 19 (busy) and 20 (tail) sums after each launch
 constexpr int kStatWords = 24;
+
+__device__ __forceinline__ unsigned tid_volatile() {
+    unsigned t;
+    asm volatile("mov.u32 %0, %%tid.x;" : "=r"(t));
+    return t;
+}
 
 __device__ __forceinline__ unsigned long long gtime() {
     unsigned long long t;
@@ -413,7 +423,15 @@ __global__ void __launch_bounds__(kSetupThreads, (KF & KF_LPT) ? 7 : 8) setup_ke
     if ((KF & KF_LPT) && !(KF & (KF_SEGS | KF_TRACE | KF_SPH))) {
         // one 32-ray tile per warp (chunks are tile aligned): file it under its cost bucket
         __syncwarp();                                  // the centre ray's segments are written
-        const int b = tile_cost_bucket(S, ws, r, rs.n);
+        // the previous frame's measured duration when the caller keeps a history (temporal
+        // coherence of a frame sequence), else the centre-ray probe estimate
+        int b;
+        if (ws.tile_cost) {
+            const unsigned c = r < rs.n ? (unsigned)ws.tile_cost[r >> 5] : 0u;
+            b = min(kBuckets - 1, max(0, 25 - __clz((int)(c | 1u))));   // log2(c) - 6
+        } else {
+            b = tile_cost_bucket(S, ws, r, rs.n);
+        }
         if ((threadIdx.x & 31) == 0 && r < rs.n) {
             const unsigned slot = atomicAdd(ws.bucket_cnt + b, 1u);
             ws.tile_list[(int64_t)b * ws.n_tiles + slot] = (int)(r >> 5);
@@ -816,6 +834,8 @@ __global__ void __launch_bounds__(kMarchThreads, MERF_MARCH_MINB) march_kernel(c
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;");
     __shared__ __align__(16) FusedSmem fsm[(KF & KF_FUSED) ? 1 : 1];
+    __shared__ unsigned s_tc[kMarchThreads / 32][2];   // per warp: tile start clock, tile (history)
+    if ((threadIdx.x & 31) == 0) s_tc[threadIdx.x >> 5][1] = ~0u;
     if (KF & KF_FUSED) {
         if (threadIdx.x == 0) fsm[0].lock = 0;
         __syncthreads();
@@ -860,6 +880,14 @@ __global__ void __launch_bounds__(kMarchThreads, MERF_MARCH_MINB) march_kernel(c
             if ((KF & KF_FUSED) && tile_rbase >= 0) fused_epilogue<KF>(S, rs, out, tile_rbase, st, fsm[0]);
             int tile = 0;
             if (lane == 0) {
+                if (ws.tile_cost) {
+                    // the finished tile's duration, for the next call's dispatch order (kept in
+                    // shared memory, not in registers: the loop is at its register cap; the warp
+                    // index is re-read, not hoisted into a register across the loop)
+                    const unsigned w = tid_volatile() >> 5;
+                    if (s_tc[w][1] != ~0u)
+                        ws.tile_cost[s_tc[w][1]] = (uint16_t)min((unsigned)(clock() - s_tc[w][0]) >> 8, 65535u);
+                }
                 int t = (int)atomicAdd(ws.queue, 1u);
                 tile = t;
                 if (ws.tile_list && t < ws.n_tiles) {
@@ -874,6 +902,11 @@ __global__ void __launch_bounds__(kMarchThreads, MERF_MARCH_MINB) march_kernel(c
             tile = __shfl_sync(FULL, tile, 0);
             const unsigned base = (unsigned)tile << 5;
             tile_rbase = base;
+            if (ws.tile_cost && lane == 0) {
+                const unsigned w = tid_volatile() >> 5;
+                s_tc[w][0] = (unsigned)clock();
+                s_tc[w][1] = tile < ws.n_tiles ? (unsigned)tile : ~0u;
+            }
             if (tile >= ws.n_tiles) {
                 if ((KF & KF_COUNT) && lane == 0) atomicMin(stats + 17, gtime());
                 break;

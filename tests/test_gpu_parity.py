@@ -687,3 +687,26 @@ def test_mixed_skip_table_equals_dyadic(M, c2, cfg):
     assert stats[0]["evaluated"] == stats[1]["evaluated"] and stats[0]["density_only"] == stats[1]["density_only"]
     assert stats[1]["skips"] < stats[0]["skips"]
     assert np.array_equal(traces[0][0], traces[1][0]) and np.array_equal(traces[0][1], traces[1][1])
+
+
+def test_tile_cost_history_order_is_bit_identical(M, c2):
+    """Frame sequences: a small single-chunk call records its per-tile march durations and the
+    next call with the same W, H and views dispatches tiles longest first by them (merf_api.cu,
+    kHistMaxViews).  Dispatch order changes no ray's arithmetic: every frame of the sequence,
+    whether it ran in raster order (first frame, or after a size change) or in history order,
+    is byte-identical, and so are its counters."""
+    import torch
+    s = M.Scene(c2)
+    cams = orbit_cameras(256, W=640, H=360, indices=[5, 77])
+    frames, stats = [], []
+    for W, H, cs in ((640, 360, cams), (640, 360, cams), (320, 180, cams[:1]), (640, 360, cams), (640, 360, cams)):
+        out = torch.zeros((len(cs), H, W, 4), dtype=torch.uint8, device="cuda")
+        st = M.merf_render(s.handle, cs, W, H, out, fmt=M.MERF_RGBA_U8, stats=True)
+        torch.cuda.synchronize()
+        if W == 640:
+            frames.append(out.cpu().numpy())
+            stats.append((st["evaluated"], st["skips"], st["density_only"]))
+    s.close()
+    for f, t in zip(frames[1:], stats[1:]):
+        assert np.array_equal(f, frames[0])
+        assert t == stats[0]
