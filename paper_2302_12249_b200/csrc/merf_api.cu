@@ -714,7 +714,8 @@ static merf_status render_frames(const merf_scene* s, const merf_camera* cams, i
     int* const lists = ws.tile_list;
     if (!cost_order(vpc)) ws.tile_list = nullptr;
     // frame-sequence history (see kHistMaxViews): one chunk, small, full frames
-    if (tile_order_override() == 0 && n_cams <= vpc && vpc <= kHistMaxViews && !prog && !shard) {
+    if (tile_order_override() == 0 && n_cams <= vpc && vpc <= kHistMaxViews && !prog && !shard &&
+        !(flags & MERF_SPHERICAL)) {     // (the spherical variant's march records nothing)
         merf_scene* ms = const_cast<merf_scene*>(s);
         std::lock_guard<std::mutex> g(ms->hmu);
         const int64_t nt = (int64_t)ws_tiles(rays_per_view * n_cams);
@@ -731,6 +732,7 @@ static merf_status render_frames(const merf_scene* s, const merf_camera* cams, i
                 cudaFreeAsync(base, st);
                 return fail(MERF_ENOMEM, "tile-cost history allocation failed");
             }
+            CUDA_TRY(cudaMemsetAsync(ms->hist, 0, (size_t)nt * sizeof(uint16_t), st));
             ms->hist_cap = nt;
         }
         const bool match = ms->hist_valid && ms->hist_W == W && ms->hist_H == H && ms->hist_views == n_cams;
