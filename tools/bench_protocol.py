@@ -3,7 +3,9 @@ fixed camera pose per configuration, identical intrinsics, the average frame rat
 frames (after 10 warm-up frames), progressive rendering off.  Each frame is ONE merf_render
 call for one view (RGBA8, device output), i.e. interactive single-frame latency -- unlike
 bench.py, which renders batches of 16 moving orbit views per call.  Times are CUDA events on
-the render stream around the 150 calls.
+the render stream around the 150 calls.  From the second call of a pose on, the library
+dispatches tiles longest first by the previous frame's measured tile costs (frame-sequence
+tile order; output byte-identical); MERF_TILE_ORDER=raster times raster order.
 
   python tools/bench_protocol.py [--frames 150] [--out profiles/r01_protocol.jsonl]
 
