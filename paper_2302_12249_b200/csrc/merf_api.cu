@@ -507,7 +507,7 @@ static int seg_slots_for(const merf_camera* cams, int n) {
 // view, so the call is 0.5-3 % slower at every batch size from 1 to 16 views.  (An earlier
 // policy used it for <= 4 views on a measurement that predates the setup-instance split.)
 static const int kLptMaxViews = 0;
-static const int kHistMaxViews = 8;
+static const int kHistMaxViews = 4;
 static bool fused_mlp() {
     static const bool v = [] { const char* e = getenv("MERF_FUSED_MLP"); return e && e[0] == '1'; }();
     return v;
