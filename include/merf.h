@@ -192,7 +192,7 @@ merf_status merf_scene_block_index(const merf_scene *scene, int32_t *index_out, 
  *   flags  MERF_NO_EARLY_TERM | MERF_COUNTERS | MERF_DENSE.
  *   stats  [host] optional; if non-NULL the call enables counters, synchronises `stream`
  *          and fills *stats (so it is no longer asynchronous).
- * Scheduling state: a call of at most 8 views in one chunk records its per-tile march
+ * Scheduling state: a call of at most 4 views in one chunk records its per-tile march
  * durations in the scene (a few hundred KB of device memory, allocated on first use); the
  * next such call with the same W, H and n_cams dispatches its tiles longest first by them.
  * Only the order in which warps take tiles changes, never a pixel (results are byte-identical

@@ -1,7 +1,7 @@
 """Per-view cost of the pipeline kernels against the number of views per merf_render call
 (the same 1080p orbit view repeated n times, and n distinct orbit views): separates the
 per-launch fixed cost (persistent march ramp and tail, launch gaps) from the per-view cost.
-Each configuration is rendered repeatedly, so calls of <= 8 views run with the frame-sequence
+Each configuration is rendered repeatedly, so calls of <= 4 views run with the frame-sequence
 tile order; MERF_TILE_ORDER=raster measures raster order.
 
   python tools/view_scaling.py [--reps 20] [--out FILE]
