@@ -58,7 +58,10 @@ def main():
                       "mean_evaluated_samples_per_ray": st["evaluated"] / rays,
                       "density_only_fraction": st["density_only"] / max(st["evaluated"], 1),
                       "protocol": "PAPER P:583: fixed pose, identical intrinsics, average over "
-                                  f"{a.frames} frames after {a.warmup} warm-up, progressive off"})
+                                  f"{a.frames} frames after {a.warmup} warm-up, progressive off",
+                      "tile_order": ("raster (MERF_TILE_ORDER=raster)" if os.environ.get("MERF_TILE_ORDER") == "raster"
+                                     else "frame-sequence history: tiles dispatched longest first by the previous "
+                                          "frame's measured tile durations (output byte-identical to raster)")})
         print(json.dumps(lines[-1]), flush=True)
     s.close()
     if a.out:
