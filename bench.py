@@ -524,7 +524,7 @@ def main():
                        "parallelism": f"views sharded over {world} rank(s), scene replicated, "
                                       "NCCL frame gather to rank 0",
                        "tile_order": ("raster" if V > 4 or os.environ.get("MERF_TILE_ORDER") == "raster" else
-                                      "frame-sequence history (views repeat every %d steps)" % (N_ORBIT // V)),
+                                      "frame-sequence history: the previous step's tile durations (other views)"),
                        "dtype_detail": "u8 features; fp64 ray setup; int32 lattice; interpolation with 16-bit "
                                        "fixed-point weights (dp2a integer sums, exact partition); fp32 decode, "
                                        "composite and MLP accumulation; MLP operands split-fp16 mma.sync"},
