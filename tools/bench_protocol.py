@@ -20,6 +20,16 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 
+def protocol_poses():
+    """(name, camera, W, H) of the protocol's four poses (shared with single_view_timed.py)"""
+    from merf_inputs import config_cameras, orbit_cameras
+    c2, W2, H2 = config_cameras("c2")
+    c3, W3, H3 = config_cameras("c3")
+    return [("c2_720p", c2[0], W2, H2), ("c3a_1080p_outward", c3[0], W3, H3),
+            ("c3b_1080p_outside_cube", c3[1], W3, H3),
+            ("orbit0_1080p", orbit_cameras(256, indices=[0])[0], 1920, 1080)]
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--frames", type=int, default=150)
@@ -30,11 +40,7 @@ def main():
     from merf_inputs import make_scene, config_cameras, orbit_cameras
     import paper_2302_12249_b200 as M
     s = M.Scene(make_scene("c2"))
-    c2, W2, H2 = config_cameras("c2")
-    c3, W3, H3 = config_cameras("c3")
-    poses = [("c2_720p", c2[0], W2, H2), ("c3a_1080p_outward", c3[0], W3, H3),
-             ("c3b_1080p_outside_cube", c3[1], W3, H3),
-             ("orbit0_1080p", orbit_cameras(256, indices=[0])[0], 1920, 1080)]
+    poses = protocol_poses()
     stream = torch.cuda.Stream()
     lines = []
     for name, cam, W, H in poses:
